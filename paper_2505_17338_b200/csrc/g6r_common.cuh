@@ -1,0 +1,121 @@
+// g6r_common.cuh -- shared device helpers for the sm_100a 6DGS render path.
+//
+// The whole library is compiled with -fmad=false: every floating-point
+// expression below rounds after each operation exactly like the reference's
+// -ffp-contract=off CPU build (pkg/setup.py:13).  Where a fused multiply-add
+// is intended it is written explicitly (__fma_rn).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/g6r.h"
+
+namespace g6r {
+
+constexpr int kBlock = 256;          // threads per CTA for streaming kernels
+constexpr int kMaxPasses = 8;        // radix passes (8-bit digits over <= 64-bit keys)
+constexpr int kSortItems = 16;       // keys per thread in a onesweep tile
+constexpr int kSortTile = kBlock * kSortItems;   // 4096 keys per tile
+constexpr double kMinAlpha = 1.0 / 255.0;        // raster.py:47
+
+// internal counter slots (int64) at the head of every workspace
+enum {
+    kTicketProject = 0,
+    kTicketSortBase = 1,   // 1..8: one per radix pass
+    kNumInternal = 16
+};
+
+// Per-splat compositing payload (f32): (mx, my, conic_a, conic_b),
+// (conic_c, alpha, r, g), (b, -, -, -).  48 bytes, 16-byte aligned.
+struct PayloadF32 {
+    float4 a, b, c;
+};
+// f64 payload: 9 doubles padded to 80 bytes (5 x double2).
+struct PayloadF64 {
+    double2 a, b, c, d, e;   // (mx,my) (ca,cb) (cc,alpha) (r,g) (b,-)
+};
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// --- glibc-compatible expf --------------------------------------------------
+// glibc 2.39 computes expf in double precision: k = round(x * 32/ln2),
+// r = x*32/ln2 - k, 2^(k/32) from a 32-entry table, and a cubic in r
+// (sysdeps/ieee754/flt-32/e_expf.c, FMA build selected on x86-64-v3 hosts).
+// Reproducing that arithmetic exactly gives the reference's f32 compositor
+// bits (raster.py:405-408 cast the splats to f32; _kernels.pyx:29-33 calls
+// expf).  Verified against the host libm on all 2.24e9 floats in [-104, 88]
+// (tests/test_expf_model.py runs the same model on the CPU).
+// Table entries: bits(2^(i/32)) - (i << 47), i.e. the exponent field is
+// re-added from k at run time.
+#define G6R_EXPF_TABLE \
+    {0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, \
+     0x3fef9301d0125b51ull, 0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, \
+     0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull, 0x3fef06fe0a31b715ull, \
+     0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull, \
+     0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, \
+     0x3feea47eb03a5585ull, 0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, \
+     0x3feea11473eb0187ull, 0x3feea589994cce13ull, 0x3feeace5422aa0dbull, \
+     0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull, \
+     0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, \
+     0x3fef3720dcef9069ull, 0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, \
+     0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull}
+
+__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
+    const double kInvLn2N = 0x1.71547652b82fep+5;   // 32 / ln 2
+    const double kShift = 0x1.8p+52;
+    const double c0 = 0x1.c6af84b912394p-20;         // poly scaled by 32^-3
+    const double c1 = 0x1.ebfce50fac4f3p-13;         // 32^-2
+    const double c2 = 0x1.62e42ff0c52d6p-6;          // 32^-1
+    const double xd = (double)x;
+    const double z = __dmul_rn(kInvLn2N, xd);
+    double kd = __dadd_rn(z, kShift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, kShift);
+    const double r = __fma_rn(kInvLn2N, xd, -kd);
+    const unsigned long long t = tab[ki & 31ull] + (ki << 47);
+    const double s = __longlong_as_double((long long)t);
+    const double p = __fma_rn(c0, r, c1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(c2, r, 1.0);
+    y = __fma_rn(p, r2, y);
+    y = __dmul_rn(y, s);
+    return __double2float_rn(y);
+}
+
+// x86 cvttsd2si semantics for the radius cast (_kernels.pyx:346): NaN -> INT_MIN.
+__device__ __forceinline__ int32_t cast_i32_x86(double v) {
+    if (isnan(v)) return INT32_MIN;
+    return (int32_t)v;
+}
+
+// --- small block-scan helpers ---------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u32(unsigned *p, unsigned v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+}  // namespace g6r

@@ -1,0 +1,269 @@
+// g6r_composite.cu -- per-tile front-to-back alpha compositing (forward) and
+// its adjoint.
+//
+// Replaces raster.py:392-415 _composite -> _kernels.pyx:36-105
+// composite_forward (and :108-187 composite_backward).  One CTA per screen
+// tile, one thread per pixel.  Each CTA walks its depth-sorted run in batches
+// of blockDim splats: the batch's payloads are gathered once into shared
+// memory (every pixel then reads them as broadcasts) and the CTA stops as soon
+// as __syncthreads_count reports every pixel saturated (T < 1e-4).  Pixel
+// arithmetic is the reference's f32 expression order with no contraction, and
+// expf is evaluated with glibc's algorithm (g6r_common.cuh), so the f32
+// framebuffer matches the reference's bit for bit.  Nothing here is a dense
+// contraction, so it runs on the FP32/FP64 pipes, not tensor cores.
+#include <algorithm>
+
+#include "g6r_common.cuh"
+#include "g6r_internal.h"
+
+namespace g6r {
+
+__constant__ unsigned long long c_expf_tab[32] = G6R_EXPF_TABLE;
+
+template <typename Real>
+struct Px;
+
+template <>
+struct Px<float> {
+    using Payload = PayloadF32;
+    struct S {   // unpacked splat in shared memory
+        float mx, my, ca, cb, cc, alpha, r, g, b;
+    };
+    __device__ static S unpack(const Payload &p) {
+        return S{p.a.x, p.a.y, p.a.z, p.a.w, p.b.x, p.b.y, p.b.z, p.b.w, p.c.x};
+    }
+};
+template <>
+struct Px<double> {
+    using Payload = PayloadF64;
+    struct S {
+        double mx, my, ca, cb, cc, alpha, r, g, b;
+    };
+    __device__ static S unpack(const Payload &p) {
+        return S{p.a.x, p.a.y, p.b.x, p.b.y, p.c.x, p.c.y, p.d.x, p.d.y, p.e.x};
+    }
+};
+
+__device__ __forceinline__ float splat_exp(float x, const unsigned long long *tab) {
+    return expf_glibc(x, tab);
+}
+__device__ __forceinline__ double splat_exp(double x, const unsigned long long *) { return exp(x); }
+
+template <typename Real>
+__global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__restrict__ payload,
+                            const unsigned *__restrict__ vals, const int64_t *__restrict__ starts,
+                            Real *__restrict__ image, Real *__restrict__ final_t,
+                            int32_t *__restrict__ last_contrib) {
+    using S = typename Px<Real>::S;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S *sp = reinterpret_cast<S *>(smem_raw);
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
+
+    const int ts = vp.tile_size;
+    const int tile = blockIdx.x;
+    const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
+    const int px = tx * ts + (int)threadIdx.x % ts;
+    const int py = ty * ts + (int)threadIdx.x / ts;
+    const bool inside = px < vp.iw && py < vp.ih;
+    const int64_t lo = starts[tile], hi = starts[tile + 1];
+    const Real fx = (Real)px, fy = (Real)py;
+    const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
+    const Real half = (Real)-0.5, one = (Real)1;
+    Real T = one, ar = 0, ag = 0, ab = 0, aa = 0;
+    int last = 0;
+    bool done = !inside;
+    const int nb = blockDim.x;
+    for (int64_t b0 = lo; b0 < hi; b0 += nb) {
+        __syncthreads();   // previous batch fully consumed (and s_tab ready)
+        const int64_t e = b0 + threadIdx.x;
+        if (e < hi) sp[threadIdx.x] = Px<Real>::unpack(payload[vals[e]]);
+        __syncthreads();
+        const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
+        if (!done) {
+            for (int j = 0; j < cnt; ++j) {
+                const S s = sp[j];
+                const Real dx = fx - s.mx;
+                const Real dy = fy - s.my;
+                const Real pw = half * (s.ca * dx * dx + s.cc * dy * dy) - s.cb * dx * dy;
+                if (pw > (Real)0 || pw < skip_lo) continue;
+                const Real ai = s.alpha * splat_exp(pw, s_tab);
+                if (ai < floor_a) continue;
+                const Real w = ai * T;
+                ar = ar + s.r * w;
+                ag = ag + s.g * w;
+                ab = ab + s.b * w;
+                aa = aa + w;
+                T = T * (one - ai);
+                last = (int)(b0 - lo) + j + 1;
+                if (T < t_stop) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+        if (__syncthreads_count(!done) == 0) break;
+    }
+    if (inside) {
+        const int64_t p = (int64_t)py * vp.iw + px;
+        if constexpr (sizeof(Real) == 4) {
+            reinterpret_cast<float4 *>(image)[p] = make_float4(ar, ag, ab, aa);
+        } else {
+            reinterpret_cast<double2 *>(image)[2 * p] = make_double2(ar, ag);
+            reinterpret_cast<double2 *>(image)[2 * p + 1] = make_double2(ab, aa);
+        }
+        final_t[p] = T;
+        last_contrib[p] = last;
+    }
+}
+
+// Pack reference-shaped splat arrays (raster.py:405-408) into payloads.
+template <typename Real>
+__global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conics, const Real *colors,
+                               const Real *alphas, typename Px<Real>::Payload *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    if constexpr (sizeof(Real) == 4) {
+        PayloadF32 p;
+        p.a = make_float4(means2d[2 * i], means2d[2 * i + 1], conics[3 * i], conics[3 * i + 1]);
+        p.b = make_float4(conics[3 * i + 2], alphas[i], colors[3 * i], colors[3 * i + 1]);
+        p.c = make_float4(colors[3 * i + 2], 0.f, 0.f, 0.f);
+        out[i] = p;
+    } else {
+        PayloadF64 p;
+        p.a = make_double2(means2d[2 * i], means2d[2 * i + 1]);
+        p.b = make_double2(conics[3 * i], conics[3 * i + 1]);
+        p.c = make_double2(conics[3 * i + 2], alphas[i]);
+        p.d = make_double2(colors[3 * i], colors[3 * i + 1]);
+        p.e = make_double2(colors[3 * i + 2], 0.0);
+        out[i] = p;
+    }
+}
+
+// Adjoint (f64), one thread per pixel, reverse sweep from last_contrib with
+// the running transmittance rebuilt by division (_kernels.pyx:135-187).  Each
+// pixel adds into the rows of the entries it touched; entries are shared by
+// the pixels of one tile only, so the adds are CTA-local shared-memory-free
+// atomics on distinct (entry, slot) addresses.
+__global__ void k_composite_backward(ViewParams vp, const double *__restrict__ means2d,
+                                     const double *__restrict__ conics, const double *__restrict__ colors,
+                                     const double *__restrict__ alphas, const int32_t *__restrict__ entry_splat,
+                                     const int64_t *__restrict__ starts, const double *__restrict__ final_t,
+                                     const int32_t *__restrict__ last_contrib,
+                                     const double *__restrict__ grad_image, double *entry_grads) {
+    const int ts = vp.tile_size;
+    const int tile = blockIdx.x;
+    const int px = (tile % vp.tiles_x) * ts + (int)threadIdx.x % ts;
+    const int py = (tile / vp.tiles_x) * ts + (int)threadIdx.x / ts;
+    if (px >= vp.iw || py >= vp.ih) return;
+    const int64_t p = (int64_t)py * vp.iw + px;
+    const int last = last_contrib[p];
+    if (last == 0) return;
+    const double gr = grad_image[4 * p], gg = grad_image[4 * p + 1];
+    const double gb = grad_image[4 * p + 2], ga = grad_image[4 * p + 3];
+    if (gr == 0.0 && gg == 0.0 && gb == 0.0 && ga == 0.0) return;
+    const int64_t lo = starts[tile];
+    const double fx = (double)px, fy = (double)py;
+    double T = final_t[p];
+    double sr = 0.0, sg = 0.0, sb = 0.0, sa = 0.0;
+    for (int64_t e = lo + last - 1; e >= lo; --e) {
+        const int64_t s = entry_splat[e];
+        const double dx = fx - means2d[2 * s];
+        const double dy = fy - means2d[2 * s + 1];
+        const double qa = conics[3 * s], qb = conics[3 * s + 1], qc = conics[3 * s + 2];
+        const double pw = -0.5 * (qa * dx * dx + qc * dy * dy) - qb * dx * dy;
+        if (pw > 0.0 || pw < -4.5) continue;
+        const double ge = exp(pw);
+        const double ai = alphas[s] * ge;
+        if (ai < 1.0 / 255.0) continue;
+        const double om = 1.0 - ai;
+        T = T / om;
+        const double w = ai * T;
+        const double *col = colors + 3 * s;
+        double *eg = entry_grads + 9 * e;
+        atomicAdd(eg + 5, w * gr);
+        atomicAdd(eg + 6, w * gg);
+        atomicAdd(eg + 7, w * gb);
+        const double dai = T * (col[0] * gr + col[1] * gg + col[2] * gb + ga) -
+                           (sr * gr + sg * gg + sb * gb + sa * ga) / om;
+        atomicAdd(eg + 8, ge * dai);
+        const double dp = ai * dai;
+        atomicAdd(eg + 0, dp * (qa * dx + qb * dy));
+        atomicAdd(eg + 1, dp * (qc * dy + qb * dx));
+        atomicAdd(eg + 2, dp * (-0.5 * dx * dx));
+        atomicAdd(eg + 3, dp * (-dx * dy));
+        atomicAdd(eg + 4, dp * (-0.5 * dy * dy));
+        sr = sr + col[0] * w;
+        sg = sg + col[1] * w;
+        sb = sb + col[2] * w;
+        sa = sa + w;
+    }
+}
+
+__global__ void k_debug_expf(int64_t n, const float *x, float *y) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = expf_glibc(x[i], s_tab);
+}
+
+int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    k_debug_expf<<<(unsigned)std::min<int64_t>(ceil_div(n, kBlock), 148 * 16), kBlock, 0, st>>>(n, x, y);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
+                        const void *colors, const void *alphas, void *payload, cudaStream_t st) {
+    if (m == 0) return G6R_OK;
+    const unsigned grid = (unsigned)ceil_div(m, kBlock);
+    if (precision)
+        k_pack_payload<double><<<grid, kBlock, 0, st>>>(
+            m, (const double *)means2d, (const double *)conics, (const double *)colors,
+            (const double *)alphas, (PayloadF64 *)payload);
+    else
+        k_pack_payload<float><<<grid, kBlock, 0, st>>>(
+            m, (const float *)means2d, (const float *)conics, (const float *)colors,
+            (const float *)alphas, (PayloadF32 *)payload);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_composite(const ViewParams &vp, const void *payload, const unsigned *entry_vals,
+                     const int64_t *tile_starts, void *image, void *final_t, int32_t *last_contrib,
+                     cudaStream_t st) {
+    const int threads = vp.tile_size * vp.tile_size;
+    const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
+    if (grid == 0) return G6R_OK;
+    if (vp.precision) {
+        const size_t smem = threads * sizeof(Px<double>::S);
+        k_composite<double><<<grid, threads, smem, st>>>(vp, (const PayloadF64 *)payload, entry_vals,
+                                                         tile_starts, (double *)image,
+                                                         (double *)final_t, last_contrib);
+    } else {
+        const size_t smem = threads * sizeof(Px<float>::S);
+        k_composite<float><<<grid, threads, smem, st>>>(vp, (const PayloadF32 *)payload, entry_vals,
+                                                        tile_starts, (float *)image,
+                                                        (float *)final_t, last_contrib);
+    }
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_composite_backward(int64_t m, const double *means2d, const double *conics,
+                              const double *colors, const double *alphas,
+                              const int32_t *entry_splat, const int64_t *tile_starts,
+                              const ViewParams &vp, const double *final_t,
+                              const int32_t *last_contrib, const double *grad_image,
+                              double *entry_grads, cudaStream_t st) {
+    (void)m;
+    const int threads = vp.tile_size * vp.tile_size;
+    const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
+    if (grid == 0) return G6R_OK;
+    k_composite_backward<<<grid, threads, 0, st>>>(vp, means2d, conics, colors, alphas, entry_splat,
+                                                   tile_starts, final_t, last_contrib, grad_image,
+                                                   entry_grads);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+}  // namespace g6r

@@ -1,0 +1,559 @@
+// g6r_project.cu -- per-view slice + EWA projection + cull + compaction +
+// tile duplication, fused into one pass over the scene.
+//
+// Replaces, for one view:
+//   raster.py:229-288  _project_rows (stage1 -> opacity modulation -> stage2 ->
+//                      fate bincount -> compaction to kept rows, ascending)
+//   _kernels.pyx:190-229 project_stage1, :232-363 project_stage2
+//   raster.py:340-375  bin_splats up to the key build (rects, counts, offsets,
+//                      duplication in splat order, key = tile<<32 | f32 depth)
+// One thread per Gaussian reads its 352-byte prepared record as 22 coalesced
+// 16-byte column loads (loaded lazily: culled rows stop early).  The compaction
+// index and the entry offset come from one decoupled-lookback scan across
+// CTAs, so the whole stage is a single launch with no host round trip.  All
+// arithmetic is IEEE double with the reference's association (-fmad=false);
+// the only transcendental, exp(-q/2), is CUDA's correctly-rounded-to-1ulp exp.
+#include "g6r_common.cuh"
+#include "g6r_internal.h"
+
+namespace g6r {
+
+struct Splat {
+    double u, v;            // means2d
+    double ca, cb, cc;      // conic (a, b, c)
+    double r, g, b;         // clamped SH colour
+    double alpha, depth;
+    int32_t rx, ry;
+};
+
+// project_stage1 for one row (_kernels.pyx:200-229).  prec6 = (00,11,22,01,02,12).
+__device__ __forceinline__ int slice_row(const double *mp, const double *md, const double *A,
+                                         const double *Q6, double px, double py, double pz,
+                                         double *view, double *madj, double &quad) {
+    const double ex = mp[0] - px, ey = mp[1] - py, ez = mp[2] - pz;
+    const double len = sqrt(ex * ex + ey * ey + ez * ez);
+    if (!(len > 1e-12)) return 1;
+    const double rl = 1.0 / len;
+    view[0] = ex * rl;
+    view[1] = ey * rl;
+    view[2] = ez * rl;
+    const double g0 = view[0] - md[0], g1 = view[1] - md[1], g2 = view[2] - md[2];
+    madj[0] = mp[0] + (A[0] * g0 + A[1] * g1 + A[2] * g2);
+    madj[1] = mp[1] + (A[3] * g0 + A[4] * g1 + A[5] * g2);
+    madj[2] = mp[2] + (A[6] * g0 + A[7] * g1 + A[8] * g2);
+    const double diag = Q6[0] * g0 * g0 + Q6[1] * g1 * g1 + Q6[2] * g2 * g2;
+    const double off = Q6[3] * g0 * g1 + Q6[4] * g0 * g2 + Q6[5] * g1 * g2;
+    quad = diag + 2.0 * off;
+    return 0;
+}
+
+__device__ __forceinline__ double clamp01(double c) {
+    if (c < 0.0) return 0.0;
+    if (c > 1.0) return 1.0;
+    return c;
+}
+
+// project_stage2 for one row (_kernels.pyx:256-363).  Returns the stage code.
+__device__ __forceinline__ int project_row(const double *view, const double *madj,
+                                           const double *sh, const double *S,
+                                           const ViewParams &vp, double sh_c0, double sh_c1,
+                                           Splat &o) {
+    const double *R = vp.rot;
+    const double wx = madj[0] - vp.pos[0], wy = madj[1] - vp.pos[1], wz = madj[2] - vp.pos[2];
+    const double tx = R[0] * wx + R[1] * wy + R[2] * wz;
+    const double ty = R[3] * wx + R[4] * wy + R[5] * wz;
+    const double tz = R[6] * wx + R[7] * wy + R[8] * wz;
+    if (!(tz >= vp.znear && tz <= vp.zfar)) return 3;
+    o.r = clamp01(sh_c0 * sh[0] - sh_c1 * view[1] * sh[3] + sh_c1 * view[2] * sh[6]
+                  - sh_c1 * view[0] * sh[9] + 0.5);
+    o.g = clamp01(sh_c0 * sh[1] - sh_c1 * view[1] * sh[4] + sh_c1 * view[2] * sh[7]
+                  - sh_c1 * view[0] * sh[10] + 0.5);
+    o.b = clamp01(sh_c0 * sh[2] - sh_c1 * view[1] * sh[5] + sh_c1 * view[2] * sh[8]
+                  - sh_c1 * view[0] * sh[11] + 0.5);
+    const double f = vp.focal;
+    const double iz = 1.0 / tz;
+    const double u = f * tx * iz + vp.cx;
+    const double v = f * ty * iz + vp.cy;
+    double xs = tx * iz;
+    if (xs < -vp.lim_x) xs = -vp.lim_x;
+    else if (xs > vp.lim_x) xs = vp.lim_x;
+    xs = xs * tz;
+    double ys = ty * iz;
+    if (ys < -vp.lim_y) ys = -vp.lim_y;
+    else if (ys > vp.lim_y) ys = vp.lim_y;
+    ys = ys * tz;
+    const double j00 = f * iz;
+    const double j02 = -f * xs * iz * iz;
+    const double j12 = -f * ys * iz * iz;
+    double B[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        B[r][0] = S[3 * r] * R[0] + S[3 * r + 1] * R[1] + S[3 * r + 2] * R[2];
+        B[r][1] = S[3 * r] * R[3] + S[3 * r + 1] * R[4] + S[3 * r + 2] * R[5];
+        B[r][2] = S[3 * r] * R[6] + S[3 * r + 1] * R[7] + S[3 * r + 2] * R[8];
+    }
+    const double m00 = R[0] * B[0][0] + R[1] * B[1][0] + R[2] * B[2][0];
+    const double m01 = R[0] * B[0][1] + R[1] * B[1][1] + R[2] * B[2][1];
+    const double m02 = R[0] * B[0][2] + R[1] * B[1][2] + R[2] * B[2][2];
+    const double m11 = R[3] * B[0][1] + R[4] * B[1][1] + R[5] * B[2][1];
+    const double m12 = R[3] * B[0][2] + R[4] * B[1][2] + R[5] * B[2][2];
+    const double m22 = R[6] * B[0][2] + R[7] * B[1][2] + R[8] * B[2][2];
+    const double k00 = j00 * m00 + j02 * m02;
+    const double k01 = j00 * m01 + j02 * m12;
+    const double k02 = j00 * m02 + j02 * m22;
+    const double k11 = j00 * m11 + j12 * m12;
+    const double k12 = j00 * m12 + j12 * m22;
+    const double ca = k00 * j00 + k02 * j02 + vp.low_pass;
+    const double cb = k01 * j00 + k02 * j12;
+    const double cc = k11 * j00 + k12 * j12 + vp.low_pass;
+    const double det = ca * cc - cb * cb;
+    if (!(isfinite(det) && det > 0.0 && isfinite(u) && isfinite(v))) return 4;
+    const double idet = 1.0 / det;
+    double rx = ceil(3.0 * sqrt(ca));
+    if (rx > 1048576.0) rx = 1048576.0;
+    double ry = ceil(3.0 * sqrt(cc));
+    if (ry > 1048576.0) ry = 1048576.0;
+    const int32_t irx = cast_i32_x86(rx), iry = cast_i32_x86(ry);
+    if (!(u + (double)irx >= 0.0 && u - (double)irx <= vp.width - 1.0 &&
+          v + (double)iry >= 0.0 && v - (double)iry <= vp.height - 1.0))
+        return 5;
+    o.u = u;
+    o.v = v;
+    o.ca = cc * idet;
+    o.cb = -cb * idet;
+    o.cc = ca * idet;
+    o.depth = tz;
+    o.rx = irx;
+    o.ry = iry;
+    return 0;
+}
+
+// Tile rectangle of a splat (raster.py:359-364), f64 floor then clip.
+__device__ __forceinline__ void tile_rect(double u, double v, int32_t rx, int32_t ry,
+                                          const ViewParams &vp, int &x0, int &y0, int &wx,
+                                          int &hy) {
+    const double ts = (double)vp.tile_size;
+    long long a = (long long)floor((u - (double)rx) / ts);
+    long long b = (long long)floor((u + (double)rx) / ts);
+    long long c = (long long)floor((v - (double)ry) / ts);
+    long long d = (long long)floor((v + (double)ry) / ts);
+    const long long mx = vp.tiles_x - 1, my = vp.tiles_y - 1;
+    a = a < 0 ? 0 : (a > mx ? mx : a);
+    b = b < 0 ? 0 : (b > mx ? mx : b);
+    c = c < 0 ? 0 : (c > my ? my : c);
+    d = d < 0 ? 0 : (d > my ? my : d);
+    x0 = (int)a;
+    y0 = (int)c;
+    wx = (int)(b - a + 1);
+    hy = (int)(d - c + 1);
+}
+
+constexpr unsigned long long kFlagReady = 1ull << 63;
+constexpr unsigned long long kValMask = kFlagReady - 1;
+
+// Decoupled look-back over CTAs carrying two sums (splats, entries).
+// Returns this CTA's exclusive prefix (pm, pe) in shared memory.
+__device__ __forceinline__ void lookback2(int64_t tile, long long bm, long long be,
+                                          const Workspace &ws, long long *s_pm,
+                                          long long *s_pe) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
+    if (tile == 0) {
+        if (lane == 0) {
+            st_volatile_u64(ws.proj_inc_e, (unsigned long long)be);
+            __threadfence();
+            st_volatile_u64(ws.proj_inc_m, kFlagReady | (unsigned long long)bm);
+            *s_pm = 0;
+            *s_pe = 0;
+        }
+        return;
+    }
+    if (lane == 0) {
+        st_volatile_u64(ws.proj_agg_e + tile, (unsigned long long)be);
+        __threadfence();
+        st_volatile_u64(ws.proj_agg_m + tile, kFlagReady | (unsigned long long)bm);
+    }
+    long long pm = 0, pe = 0;
+    int64_t j0 = tile - 1;
+    while (true) {
+        const int64_t j = j0 - lane;
+        unsigned long long mw = kFlagReady, ev = 0;
+        bool inc = true;
+        if (j >= 0) {
+            while (true) {
+                unsigned long long w = ld_volatile_u64(ws.proj_inc_m + j);
+                if (w) {
+                    __threadfence();
+                    ev = ld_volatile_u64(ws.proj_inc_e + j);
+                    mw = w;
+                    inc = true;
+                    break;
+                }
+                w = ld_volatile_u64(ws.proj_agg_m + j);
+                if (w) {
+                    __threadfence();
+                    ev = ld_volatile_u64(ws.proj_agg_e + j);
+                    mw = w;
+                    inc = false;
+                    break;
+                }
+            }
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, inc);
+        const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
+        long long cm = lane <= first ? (long long)(mw & kValMask) : 0;
+        long long ce = lane <= first ? (long long)ev : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cm += __shfl_xor_sync(0xffffffffu, cm, o);
+            ce += __shfl_xor_sync(0xffffffffu, ce, o);
+        }
+        pm += cm;
+        pe += ce;
+        if (inc_mask) break;
+        j0 -= 32;
+    }
+    if (lane == 0) {
+        st_volatile_u64(ws.proj_inc_e + tile, (unsigned long long)(pe + be));
+        __threadfence();
+        st_volatile_u64(ws.proj_inc_m + tile, kFlagReady | (unsigned long long)(pm + bm));
+        *s_pm = pm;
+        *s_pe = pe;
+    }
+}
+
+// Block-wide exclusive scan of two ints; returns totals in *tot_a/*tot_b.
+__device__ __forceinline__ void block_scan2(int a, int b, int &ea, int &eb, int *s_wa, int *s_wb,
+                                            int &tot_a, int &tot_b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ia = warp_inclusive_scan(a);
+    const int ib = warp_inclusive_scan(b);
+    if (lane == 31) {
+        s_wa[warp] = ia;
+        s_wb[warp] = ib;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        int va = lane < nw ? s_wa[lane] : 0;
+        int vb = lane < nw ? s_wb[lane] : 0;
+        const int sa = warp_inclusive_scan(va);
+        const int sb = warp_inclusive_scan(vb);
+        if (lane < nw) {
+            s_wa[lane] = sa - va;
+            s_wb[lane] = sb - vb;
+        }
+        if (lane == nw - 1) {
+            s_wa[32] = sa;
+            s_wb[32] = sb;
+        }
+    }
+    __syncthreads();
+    ea = s_wa[warp] + ia - a;
+    eb = s_wb[warp] + ib - b;
+    tot_a = s_wa[32];
+    tot_b = s_wb[32];
+}
+
+// Cooperative duplication of this CTA's kept splats into (key, value) entries,
+// in ascending splat order with tiles row-major inside each rect (the order
+// np.repeat produces in raster.py:369-375).
+__device__ __forceinline__ void emit_entries(int nk, int ne, long long m_base, long long e_base,
+                                             const int *s_eoff, const int *s_x0, const int *s_y0,
+                                             const int *s_wx, const unsigned *s_db,
+                                             const ViewParams &vp, unsigned long long *keys,
+                                             unsigned *vals) {
+    for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+        int lo = 0, hi = nk - 1;   // largest l with s_eoff[l] <= j
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_eoff[mid] <= j) lo = mid;
+            else hi = mid - 1;
+        }
+        const int loc = j - s_eoff[lo];
+        const int w = s_wx[lo];
+        const int ty = s_y0[lo] + loc / w;
+        const int tx = s_x0[lo] + loc % w;
+        const unsigned long long tile = (unsigned long long)ty * (unsigned)vp.tiles_x + (unsigned)tx;
+        keys[e_base + j] = (tile << 32) | s_db[lo];
+        vals[e_base + j] = (unsigned)(m_base + lo);
+    }
+}
+
+template <bool kF64>
+__global__ void __launch_bounds__(kBlock)
+k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *counters,
+          g6r_splat_out so, int write_entries, double sh_c0, double sh_c1) {
+    __shared__ int s_tile;
+    __shared__ int s_wa[33], s_wb[33];
+    __shared__ long long s_pm, s_pe;
+    __shared__ unsigned s_fate[6];
+    __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
+    __shared__ unsigned s_db[kBlock];
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
+    if (threadIdx.x < 6) s_fate[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t n = scene.n;
+    const int64_t i = tile * kBlock + threadIdx.x;
+    const double2 *rec = reinterpret_cast<const double2 *>(scene.records);
+
+    int st = 255;
+    Splat o;
+    int x0 = 0, y0 = 0, wx = 0, hy = 0;
+    if (i < n) {
+        const unsigned fl = scene.flags[i];
+        if (((mask >> (fl & 15u)) & 1u) && !(fl & G6R_FLAG_DEGENERATE)) {
+            double r[G6R_REC_DOUBLES];
+#pragma unroll
+            for (int c = 0; c < 11; ++c) {   // mu_p, mu_d, adjust, precision_dd
+                const double2 q = __ldg(&rec[c * n + i]);
+                r[2 * c] = q.x;
+                r[2 * c + 1] = q.y;
+            }
+            double view[3], madj[3], quad;
+            st = slice_row(r + 0, r + 3, r + 6, r + 15, vp.pos[0], vp.pos[1], vp.pos[2], view, madj,
+                           quad);
+            if (st == 0) {
+                const double2 q = __ldg(&rec[21 * n + i]);   // opacity, w_norm
+                const double w = exp(-0.5 * quad) * q.y;
+                double alpha = q.x * w;
+                alpha = alpha > vp.alpha_max ? vp.alpha_max : alpha;   // np.minimum (NaN stays)
+                o.alpha = alpha;
+                if (!(alpha >= kMinAlpha)) st = 2;
+            }
+            if (st == 0) {
+#pragma unroll
+                for (int c = 11; c < 21; ++c) {   // sigma_prime (tail of col 10 already read), sh
+                    const double2 q = __ldg(&rec[c * n + i]);
+                    r[2 * c] = q.x;
+                    r[2 * c + 1] = q.y;
+                }
+                st = project_row(view, madj, r + 30, r + 21, vp, sh_c0, sh_c1, o);
+            }
+            if (st == 0) tile_rect(o.u, o.v, o.rx, o.ry, vp, x0, y0, wx, hy);
+        }
+        if (so.stage) so.stage[i] = (uint8_t)st;
+    }
+    if (st < 6) atomicAdd(&s_fate[st], 1u);
+    const int kept = st == 0;
+    const int cnt = kept ? wx * hy : 0;
+    int lm, le, bm, be;
+    block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
+    lookback2(tile, bm, be, ws, &s_pm, &s_pe);
+    __syncthreads();
+    const long long m_base = s_pm, e_base = s_pe;
+    if (kept) {
+        const long long m = m_base + lm;
+        if (kF64) {
+            PayloadF64 p;
+            p.a = make_double2(o.u, o.v);
+            p.b = make_double2(o.ca, o.cb);
+            p.c = make_double2(o.cc, o.alpha);
+            p.d = make_double2(o.r, o.g);
+            p.e = make_double2(o.b, 0.0);
+            reinterpret_cast<PayloadF64 *>(ws.payload)[m] = p;
+        } else {
+            PayloadF32 p;
+            p.a = make_float4((float)o.u, (float)o.v, (float)o.ca, (float)o.cb);
+            p.b = make_float4((float)o.cc, (float)o.alpha, (float)o.r, (float)o.g);
+            p.c = make_float4((float)o.b, 0.f, 0.f, 0.f);
+            reinterpret_cast<PayloadF32 *>(ws.payload)[m] = p;
+        }
+        if (so.gids) so.gids[m] = i;
+        if (so.means2d) {
+            so.means2d[2 * m] = o.u;
+            so.means2d[2 * m + 1] = o.v;
+        }
+        if (so.conics) {
+            so.conics[3 * m] = o.ca;
+            so.conics[3 * m + 1] = o.cb;
+            so.conics[3 * m + 2] = o.cc;
+        }
+        if (so.colors) {
+            so.colors[3 * m] = o.r;
+            so.colors[3 * m + 1] = o.g;
+            so.colors[3 * m + 2] = o.b;
+        }
+        if (so.alphas) so.alphas[m] = o.alpha;
+        if (so.depths) so.depths[m] = o.depth;
+        if (so.radii) {
+            so.radii[2 * m] = o.rx;
+            so.radii[2 * m + 1] = o.ry;
+        }
+        s_eoff[lm] = le;
+        s_x0[lm] = x0;
+        s_y0[lm] = y0;
+        s_wx[lm] = wx;
+        s_db[lm] = __float_as_uint((float)o.depth);
+    }
+    __syncthreads();
+    if (threadIdx.x < 6 && s_fate[threadIdx.x])
+        atomicAdd((unsigned long long *)&counters[G6R_CNT_FATE + threadIdx.x],
+                  (unsigned long long)s_fate[threadIdx.x]);
+    if (write_entries) {
+        if (e_base + be <= ws.entry_capacity) {
+            emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0],
+                         ws.vals[0]);
+        } else if (threadIdx.x == 0) {
+            counters[G6R_CNT_OVERFLOW] = 1;
+        }
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+        counters[G6R_CNT_DRAWN] = m_base + bm;
+        counters[G6R_CNT_ENTRIES] = e_base + be;
+    }
+}
+
+// Binning of externally supplied splats (raster.py:340-375 on a given SplatBatch).
+__global__ void __launch_bounds__(kBlock)
+k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__restrict__ radii,
+            const double *__restrict__ depths, ViewParams vp, Workspace ws, int64_t *counters) {
+    __shared__ int s_tile;
+    __shared__ int s_wa[33], s_wb[33];
+    __shared__ long long s_pm, s_pe;
+    __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
+    __shared__ unsigned s_db[kBlock];
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t i = tile * kBlock + threadIdx.x;
+    int x0 = 0, y0 = 0, wx = 0, hy = 0;
+    const int kept = i < m;
+    if (kept) tile_rect(means2d[2 * i], means2d[2 * i + 1], radii[2 * i], radii[2 * i + 1], vp, x0, y0, wx, hy);
+    const int cnt = kept ? wx * hy : 0;
+    int lm, le, bm, be;
+    block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
+    lookback2(tile, bm, be, ws, &s_pm, &s_pe);
+    __syncthreads();
+    if (kept) {
+        s_eoff[lm] = le;
+        s_x0[lm] = x0;
+        s_y0[lm] = y0;
+        s_wx[lm] = wx;
+        s_db[lm] = __float_as_uint((float)depths[i]);
+    }
+    __syncthreads();
+    const long long m_base = s_pm, e_base = s_pe;
+    if (e_base + be <= ws.entry_capacity) {
+        emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0], ws.vals[0]);
+    } else if (threadIdx.x == 0) {
+        counters[G6R_CNT_OVERFLOW] = 1;
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+        counters[G6R_CNT_DRAWN] = m;
+        counters[G6R_CNT_ENTRIES] = e_base + be;
+    }
+}
+
+// --- kernel-module contract mirrors (uncompacted, per row) ----------------------
+__global__ void k_stage1(int64_t n, const double *mu_p, const double *mu_d, const double *adjust,
+                         const double *prec, double px, double py, double pz, double *view,
+                         double *mean_adj, double *quad, uint8_t *stage) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *Q = prec + 9 * i;
+    const double q6[6] = {Q[0], Q[4], Q[8], Q[1], Q[2], Q[5]};
+    double v[3], ma[3], q;
+    if (slice_row(mu_p + 3 * i, mu_d + 3 * i, adjust + 9 * i, q6, px, py, pz, v, ma, q)) {
+        stage[i] = 1;
+        return;
+    }
+    for (int k = 0; k < 3; ++k) {
+        view[3 * i + k] = v[k];
+        mean_adj[3 * i + k] = ma[k];
+    }
+    quad[i] = q;
+}
+
+__global__ void k_stage2(int64_t n, const double *view, const double *mean_adj, const double *sh,
+                         const double *sigma_prime, ViewParams vp, double sh_c0, double sh_c1,
+                         double *means2d, double *conics, double *colors, double *depths,
+                         int32_t *radii, uint8_t *stage) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || stage[i] != 0) return;
+    Splat o;
+    const int st = project_row(view + 3 * i, mean_adj + 3 * i, sh + 12 * i, sigma_prime + 9 * i,
+                               vp, sh_c0, sh_c1, o);
+    if (st) {
+        stage[i] = (uint8_t)st;
+        return;
+    }
+    means2d[2 * i] = o.u;
+    means2d[2 * i + 1] = o.v;
+    conics[3 * i] = o.ca;
+    conics[3 * i + 1] = o.cb;
+    conics[3 * i + 2] = o.cc;
+    colors[3 * i] = o.r;
+    colors[3 * i + 1] = o.g;
+    colors[3 * i + 2] = o.b;
+    depths[i] = o.depth;
+    radii[2 * i] = o.rx;
+    radii[2 * i + 1] = o.ry;
+}
+
+static const double kShC0 = 0.28209479177387814;   // core.py:25
+static const double kShC1 = 0.4886025119029199;    // core.py:26
+
+int launch_project(const g6r_scene &scene, uint32_t mask, const ViewParams &vp,
+                   const Workspace &ws, int64_t *counters, const g6r_splat_out *splats,
+                   bool write_entries, cudaStream_t st) {
+    g6r_splat_out so{};
+    if (splats) so = *splats;
+    if (scene.n == 0) return G6R_OK;
+    const unsigned grid = (unsigned)ceil_div(scene.n, kBlock);
+    if (vp.precision)
+        k_project<true><<<grid, kBlock, 0, st>>>(scene, mask, vp, ws, counters, so, write_entries,
+                                                  kShC0, kShC1);
+    else
+        k_project<false><<<grid, kBlock, 0, st>>>(scene, mask, vp, ws, counters, so, write_entries,
+                                                   kShC0, kShC1);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, const double *depths,
+                     const ViewParams &vp, const Workspace &ws, int64_t *counters, cudaStream_t st) {
+    if (m == 0) return G6R_OK;
+    k_duplicate<<<(unsigned)ceil_div(m, kBlock), kBlock, 0, st>>>(m, means2d, radii, depths, vp, ws,
+                                                                   counters);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_stage1(int64_t n, const double *mu_p, const double *mu_d, const double *adjust,
+                  const double *prec, double px, double py, double pz, double *view,
+                  double *mean_adj, double *quad, uint8_t *stage, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    k_stage1<<<(unsigned)ceil_div(n, kBlock), kBlock, 0, st>>>(n, mu_p, mu_d, adjust, prec, px, py,
+                                                                pz, view, mean_adj, quad, stage);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int launch_stage2(int64_t n, const double *view, const double *mean_adj, const double *sh,
+                  const double *sigma_prime, const double *rot, double px, double py, double pz,
+                  double znear, double zfar, double f, double ox, double oy, double lim_x,
+                  double lim_y, double width, double height, double low_pass, double sh_c0,
+                  double sh_c1, double *means2d, double *conics, double *colors, double *depths,
+                  int32_t *radii, uint8_t *stage, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    ViewParams vp{};
+    vp.pos[0] = px;
+    vp.pos[1] = py;
+    vp.pos[2] = pz;
+    for (int k = 0; k < 9; ++k) vp.rot[k] = rot[k];
+    vp.focal = f;
+    vp.cx = ox;
+    vp.cy = oy;
+    vp.znear = znear;
+    vp.zfar = zfar;
+    vp.lim_x = lim_x;
+    vp.lim_y = lim_y;
+    vp.width = width;
+    vp.height = height;
+    vp.low_pass = low_pass;
+    k_stage2<<<(unsigned)ceil_div(n, kBlock), kBlock, 0, st>>>(n, view, mean_adj, sh, sigma_prime,
+                                                                vp, sh_c0, sh_c1, means2d, conics,
+                                                                colors, depths, radii, stage);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+}  // namespace g6r

@@ -1,0 +1,93 @@
+"""View-parallel rendering across GPUs (one process per GPU).
+
+The render path shards naturally over camera views: once the
+Gaussian set is resident, views are independent.  So the only collective is a
+one-time broadcast of the scene's parameter SoA from the source rank
+(``torch.distributed`` with backend ``nccl`` over NVLink on B200 nodes,
+``gloo`` for CPU tests); each rank then prepares the scene locally and renders
+the contiguous block ``[g*V/G, (g+1)*V/G)`` of the orbit.  There is no
+per-view exchange and no data-path collective.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+# column layout of the packed broadcast payload (float64, N x 40)
+_COLS = (("mu_p", 3), ("mu_d", 3), ("cov_raw", 21), ("sh", 12), ("opacity_raw", 1))
+N_PARAMS = 40
+
+
+class DeviceScene:
+    """Scene whose parameter arrays already live on a device (torch tensors).
+
+    Accepted wherever the renderer takes a scene: ``prepare_scene`` uploads
+    nothing and prepares straight from these tensors."""
+
+    def __init__(self, mu_p, mu_d, cov_raw, sh, opacity_raw, labels, spatial_scale,
+                 directional_scale):
+        self.mu_p = mu_p
+        self.mu_d = mu_d
+        self.cov_raw = cov_raw
+        self.sh = sh
+        self.opacity_raw = opacity_raw
+        self.labels = labels
+        self.spatial_scale = np.asarray(spatial_scale, dtype=np.float64)
+        self.directional_scale = float(directional_scale)
+
+    def __len__(self):
+        return int(self.mu_p.shape[0])
+
+
+def shard_views(n_views: int, world: int, rank: int) -> range:
+    """Contiguous block of views owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    return range(rank * n_views // world, (rank + 1) * n_views // world)
+
+
+def pack_scene(scene, device) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """(N,40) float64 params, (N,) uint8 labels, (4,) float64 scales."""
+    params = np.concatenate([np.asarray(getattr(scene, name), dtype=np.float64).reshape(-1, w)
+                             for name, w in _COLS], axis=1)
+    scales = np.concatenate([np.broadcast_to(np.asarray(scene.spatial_scale, np.float64), (3,)),
+                             [float(scene.directional_scale)]])
+    return (torch.from_numpy(np.ascontiguousarray(params)).to(device),
+            torch.from_numpy(np.ascontiguousarray(scene.labels, dtype=np.uint8)).to(device),
+            torch.from_numpy(scales).to(device))
+
+
+def unpack_scene(params: torch.Tensor, labels: torch.Tensor, scales: torch.Tensor) -> DeviceScene:
+    cols, k = {}, 0
+    for name, w in _COLS:
+        t = params[:, k:k + w]
+        cols[name] = t.reshape(-1).contiguous() if w == 1 else t.contiguous()
+        k += w
+    sc = scales.cpu().numpy()
+    return DeviceScene(spatial_scale=sc[:3], directional_scale=sc[3], labels=labels.contiguous(),
+                       **cols)
+
+
+def broadcast_scene(scene, device, src: int = 0, group=None) -> DeviceScene:
+    """Broadcast ``scene`` (given on ``src``, ignored elsewhere) to every rank.
+
+    Three collectives in total per scene: the row count, the (N,40) float64
+    parameters plus the label bytes, and the 4 scales."""
+    rank = dist.get_rank(group)
+    n = torch.zeros(1, dtype=torch.int64, device=device)
+    if rank == src:
+        n[0] = len(scene.mu_p)
+    dist.broadcast(n, src, group=group)
+    n = int(n.item())
+    if rank == src:
+        params, labels, scales = pack_scene(scene, device)
+    else:
+        params = torch.empty((n, N_PARAMS), dtype=torch.float64, device=device)
+        labels = torch.empty(n, dtype=torch.uint8, device=device)
+        scales = torch.empty(4, dtype=torch.float64, device=device)
+    dist.broadcast(params, src, group=group)
+    dist.broadcast(labels, src, group=group)
+    dist.broadcast(scales, src, group=group)
+    return unpack_scene(params, labels, scales)

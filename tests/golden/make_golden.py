@@ -1,0 +1,111 @@
+"""Generate the golden fixtures in tests/golden from the UNMODIFIED reference.
+
+Run in the build container (the reference exists only there):
+    python tests/golden/make_golden.py
+It imports splatct from oracle/_ref (built by oracle/build_ref.sh), renders
+seeded scenes with the reference's own render_with_state, and stores inputs
+that are not regenerable from a seed plus every output the parity tests pin:
+SplatBatch, entry_splat, tile_starts, sorted keys, image/final_t/last_contrib
+(f32 and f64) and the prepared terms.  Also stores libm expf samples.
+"""
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+sys.path.insert(0, ROOT)
+
+from splatct import raster  # noqa: E402  (the reference)
+from splatct.priming import Scene as RefScene  # noqa: E402
+
+from paper_2505_17338_b200 import scenes  # noqa: E402
+
+# (name, seed, n, camera kwargs, config kwargs, mutate)
+CASES = [
+    ("rand1", 0, 1, dict(azimuth=0.0, elevation=0.0, width=48, height=40), {}),
+    ("rand40", 2, 40, dict(azimuth=0.6, elevation=0.3, width=48, height=40), {}),
+    ("rand400", 5, 400, dict(azimuth=-0.8, elevation=0.2, width=96, height=80), {}),
+    ("rand400_raw", 6, 400, dict(azimuth=1.3, elevation=-0.4, width=64, height=64),
+     dict(w_mode="raw")),
+    ("rand400_t8", 8, 400, dict(azimuth=2.2, elevation=0.1, width=70, height=50),
+     dict(tile_size=8)),
+    ("cull100", 13, 100, dict(azimuth=0.0, elevation=0.0, width=64, height=64), {}),
+    ("ties50", 14, 50, dict(azimuth=2.1, elevation=0.3, width=64, height=64), {}),
+]
+
+
+def to_ref(s):
+    return RefScene(mu_p=s.mu_p, mu_d=s.mu_d, cov_raw=s.cov_raw, sh=s.sh,
+                    opacity_raw=s.opacity_raw, labels=s.labels, spacing=s.spacing,
+                    origin=s.origin, direction=s.direction, spatial_scale=s.spatial_scale,
+                    directional_scale=s.directional_scale)
+
+
+def make_case(name, seed, n, cam_kw, cfg_kw):
+    rng = np.random.default_rng(seed)
+    box = 8.0 if name.startswith("ties") else 22.0
+    s = scenes.random_scene(rng, n, box=box, iso=name.startswith("ties"))
+    cam = scenes.orbit_camera(**cam_kw)
+    if name.startswith("cull"):
+        mu = s.mu_p.copy()
+        mu[5] = (0.0, 0.0, 200.0)
+        mu[6] = (900.0, 0.0, 0.0)
+        mu[8] = cam.position
+        op = s.opacity_raw.copy()
+        op[12] = -9.0
+        s = s.with_params(mu_p=mu, opacity_raw=op)
+    if name.startswith("ties"):
+        mu = s.mu_p.copy()
+        mu[1] = mu[0]
+        mu[3] = mu[2] * (1.0 + 1e-12)
+        mu[10:15] = mu[10]
+        s = s.with_params(mu_p=mu)
+    out = dict(mu_p=s.mu_p, mu_d=s.mu_d, cov_raw=s.cov_raw, sh=s.sh, opacity_raw=s.opacity_raw,
+               labels=s.labels, spatial_scale=s.spatial_scale,
+               directional_scale=np.float64(s.directional_scale),
+               cam_position=cam.position, cam_rotation=cam.rotation,
+               cam_fov=np.float64(cam.fov_y), cam_wh=np.array([cam.width, cam.height]))
+    rs = to_ref(s)
+    for prec in ("f32", "f64"):
+        cfg = raster.RenderConfig(precision=prec, threads=1, **cfg_kw)
+        st = raster.render_with_state(rs, cam, None, cfg)
+        out[f"{prec}_image"] = st.image
+        out[f"{prec}_final_t"] = st.final_t
+        out[f"{prec}_last_contrib"] = st.last_contrib
+    sp = st.splats
+    for f in ("gids", "means2d", "conics", "colors", "alphas", "depths", "radii"):
+        out[f"splat_{f}"] = getattr(sp, f)
+    out["entry_splat"] = st.entries.entry_splat
+    out["tile_starts"] = st.entries.tile_starts
+    out["stats"] = np.array([st.stats.n_drawn, st.stats.n_entries, st.stats.n_view_degenerate,
+                             st.stats.n_alpha_culled, st.stats.n_depth_culled,
+                             st.stats.n_projection_culled, st.stats.n_viewport_culled])
+    prep = raster.prepare_scene(rs, cfg_kw.get("w_mode", "peak"))
+    for f in ("adjust", "precision_dd", "sigma_prime", "w_norm", "degenerate"):
+        out[f"prep_{f}"] = getattr(prep.terms, f)
+    out["prep_opacity"] = prep.opacity
+    out["config"] = np.array([cfg_kw.get("tile_size", 16), 1 if cfg_kw.get("w_mode") == "raw" else 0])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "M", st.stats.n_drawn, "E", st.stats.n_entries)
+
+
+def make_expf():
+    libm = ctypes.CDLL("libm.so.6")
+    libm.expf.restype = ctypes.c_float
+    libm.expf.argtypes = [ctypes.c_float]
+    rng = np.random.default_rng(123)
+    x = np.concatenate([rng.uniform(-4.5, 0.0, 20000), -np.logspace(-8, np.log10(4.5), 2000),
+                        np.array([0.0, -4.5, -1e-30, -0.5, -1.0])]).astype(np.float32)
+    y = np.array([libm.expf(float(v)) for v in x], dtype=np.float32)
+    np.savez_compressed(os.path.join(HERE, "expf_glibc.npz"), x=x, y=y)
+
+
+if __name__ == "__main__":
+    for case in CASES:
+        make_case(*case)
+    make_expf()
