@@ -159,8 +159,11 @@ def reference_scene(scene):
 def time_reference(scene, cams, seconds, max_views):
     """Reference CPU renderer (oracle/_ref: splatct with its OpenMP kernels) on
     all host cores: prep once, one warm-up view, then views until `seconds`."""
-    if not os.path.isdir(os.path.join(ROOT, "oracle", "_ref", "splatct")):
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "splatct")):
         return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
     from splatct import raster as R
     rs = reference_scene(scene)
     cores = os.cpu_count() or 1

@@ -84,7 +84,7 @@ _SIGS = {
     "g6r_prepare": (ctypes.c_int, [I64, P, P, P, P, P, P, P, D, I32, P, P, P, P]),
     "g6r_pack_records": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P, P, P, P, P]),
     "g6r_render": (ctypes.c_int, [P, U32, P, P, P, SZ, I64, P, P, P]),
-    "g6r_render_views": (ctypes.c_int, [P, U32, P, I32, P, P, SZ, I64, P, P, P]),
+    "g6r_render_views": (ctypes.c_int, [P, U32, P, I32, P, P, SZ, I64, P, I32, P, P]),
     "g6r_profiler_create": (P, [I32]),
     "g6r_profiler_destroy": (None, [P]),
     "g6r_profiler_reset": (None, [P]),

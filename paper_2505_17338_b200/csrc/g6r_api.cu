@@ -6,7 +6,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "g6r_common.cuh"
 #include "g6r_internal.h"
@@ -158,14 +161,34 @@ static void prof_mark(g6r_profiler *p, int k, cudaStream_t st) {
     if (p && p->used < p->max_views) cudaEventRecord(p->ev[p->used * (G6R_NSTAGES + 1) + k], st);
 }
 
+constexpr int kMaxSlots = 8;
+
+// Side streams for concurrent views, created once per device and reused.
+static int side_streams(int n, cudaStream_t *out) {
+    static std::mutex mu;
+    static std::map<int, std::vector<cudaStream_t>> pool;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    std::vector<cudaStream_t> &v = pool[dev];
+    while ((int)v.size() < n) {
+        cudaStream_t s;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+            return cuda_check("cudaStreamCreate");
+        v.push_back(s);
+    }
+    for (int i = 0; i < n; ++i) out[i] = v[i];
+    return G6R_OK;
+}
+
 static int render_one(const g6r_scene *scene, uint32_t mask, const g6r_camera *cam,
                       const g6r_config *cfg, void *ws_base, size_t ws_bytes, int64_t cap,
                       const g6r_frame *fr, const g6r_splat_out *splats, cudaStream_t st,
                       g6r_profiler *prof = nullptr) {
     if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL or has negative size");
     if (scene->n > 0 && (!scene->records || !scene->flags)) return fail(G6R_EINVAL, "scene arrays are NULL");
-    if (!fr || !fr->image || !fr->final_t || !fr->last_contrib || !fr->counters)
-        return fail(G6R_EINVAL, "frame outputs image/final_t/last_contrib/counters are required");
+    if (!fr || !fr->image || !fr->counters)
+        return fail(G6R_EINVAL, "frame outputs image/counters are required");
     if (int rc = check_cap(cap)) return rc;
     ViewParams vp;
     if (int rc = make_view(cam, cfg, vp)) return rc;
@@ -249,14 +272,53 @@ int g6r_render(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *ca
 int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cams,
                      int32_t count, const g6r_config *cfg, void *workspace,
                      size_t workspace_bytes, int64_t entry_capacity, const g6r_frame *frames,
-                     g6r_profiler *prof, g6r_stream_t stream) {
+                     int32_t concurrency, g6r_profiler *prof, g6r_stream_t stream) {
     if (count < 0 || (count > 0 && (!cams || !frames))) return fail(G6R_EINVAL, "bad view list");
-    for (int32_t k = 0; k < count; ++k) {
-        const int rc = render_one(scene, group_mask, &cams[k], cfg, workspace, workspace_bytes,
-                                  entry_capacity, &frames[k], nullptr, (cudaStream_t)stream, prof);
-        if (rc) return rc;
+    if (count == 0) return G6R_OK;
+    if (!scene || !cfg) return fail(G6R_EINVAL, "scene/config is NULL");
+    if (int rc = check_config(cfg)) return rc;
+    int slots = concurrency < 1 ? 1 : (concurrency > kMaxSlots ? kMaxSlots : concurrency);
+    if (slots > count) slots = count;
+    const int64_t tiles = (int64_t)((cams[0].width + cfg->tile_size - 1) / cfg->tile_size) *
+                          ((cams[0].height + cfg->tile_size - 1) / cfg->tile_size);
+    const size_t per = layout(scene->n, tiles, entry_capacity, cfg->precision).total;
+    if (workspace_bytes < per * slots)
+        return fail(G6R_EINVAL, "workspace too small for %d concurrent views: %zu < %zu", slots,
+                    workspace_bytes, per * slots);
+    cudaStream_t main = (cudaStream_t)stream;
+    if (slots == 1) {
+        for (int32_t k = 0; k < count; ++k) {
+            const int rc = render_one(scene, group_mask, &cams[k], cfg, workspace, per,
+                                      entry_capacity, &frames[k], nullptr, main, prof);
+            if (rc) return rc;
+        }
+        return G6R_OK;
     }
-    return G6R_OK;
+    // Views are independent: spread them over `slots` side streams, each with
+    // its own workspace slice, so one view's long tile runs overlap the next
+    // view's projection and sort instead of idling the other SMs.
+    cudaStream_t side[kMaxSlots];
+    if (int rc = side_streams(slots, side)) return rc;
+    cudaEvent_t fork;
+    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return cuda_check("event");
+    cudaEventRecord(fork, main);
+    for (int s = 0; s < slots; ++s) cudaStreamWaitEvent(side[s], fork, 0);
+    cudaEventDestroy(fork);
+    int rc = G6R_OK;
+    for (int32_t k = 0; k < count && rc == G6R_OK; ++k) {
+        const int s = k % slots;
+        rc = render_one(scene, group_mask, &cams[k], cfg, static_cast<char *>(workspace) + per * s,
+                        per, entry_capacity, &frames[k], nullptr, side[s], prof);
+    }
+    for (int s = 0; s < slots; ++s) {   // join (also on error, so the streams stay ordered)
+        cudaEvent_t j;
+        if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventRecord(j, side[s]);
+            cudaStreamWaitEvent(main, j, 0);
+            cudaEventDestroy(j);
+        }
+    }
+    return rc;
 }
 
 g6r_profiler *g6r_profiler_create(int32_t max_views) {

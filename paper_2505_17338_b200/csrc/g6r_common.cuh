@@ -27,14 +27,43 @@ enum {
 };
 
 // Per-splat compositing payload (f32): (mx, my, conic_a, conic_b),
-// (conic_c, alpha, r, g), (b, -, -, -).  48 bytes, 16-byte aligned.
+// (conic_c, alpha, r, g), (b, cull_x, cull_y, -).  48 bytes, 16-byte aligned.
+// cull_x/cull_y are conservative half-extents of the region where the
+// compositor can see power >= -4.5 (see cull_extents); outside them every
+// pixel skips the splat, so whole warps may skip it without changing a bit.
 struct PayloadF32 {
     float4 a, b, c;
 };
-// f64 payload: 9 doubles padded to 80 bytes (5 x double2).
+// f64 payload: 9 doubles + the two cull extents, 96 bytes (6 x double2).
 struct PayloadF64 {
-    double2 a, b, c, d, e;   // (mx,my) (ca,cb) (cc,alpha) (r,g) (b,-)
+    double2 a, b, c, d, e;   // (mx,my) (ca,cb) (cc,alpha) (r,g) (b, cull_x)
+    double2 f;               // (cull_y, -)
 };
+
+// Half-extents (px) of {q(dx,dy) = a dx^2 + 2 b dx dy + c dy^2 <= 9} -- the
+// only pixels whose power = -q/2 can reach the [-4.5, 0] window -- inflated so
+// the test stays conservative under the compositor's float rounding.  The
+// computed q carries a relative error of at most ~10 ulp of
+// (a dx^2 + c dy^2) <= 4 kappa q, kappa = (a+c)^2 / (4 det); outside the box
+// grown by (1 + delta), delta >> 10 ulp * 4 kappa, the computed power is
+// therefore still < -4.5.  Non-positive-definite conics get an infinite box.
+__device__ __forceinline__ void cull_extents(double a, double b, double c, double ulp,
+                                             float &ex, float &ey) {
+    const double det = a * c - b * b;
+    if (!(det > 0.0) || !(a > 0.0) || !(c > 0.0)) {
+        ex = ey = __int_as_float(0x7f800000);
+        return;
+    }
+    const double kappa = (a + c) * (a + c) / (4.0 * det);
+    const double delta = 64.0 * ulp * kappa + 1e-6;
+    if (!(delta < 0.5)) {
+        ex = ey = __int_as_float(0x7f800000);
+        return;
+    }
+    const double grow = 1.0 + delta;
+    ex = (float)(3.0 * sqrt(c / det) * grow + 1e-3);
+    ey = (float)(3.0 * sqrt(a / det) * grow + 1e-3);
+}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

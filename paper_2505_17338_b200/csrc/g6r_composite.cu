@@ -29,7 +29,9 @@ struct Px<float> {
     struct S {   // unpacked splat in shared memory
         float mx, my, ca, cb, cc, alpha, r, g, b;
     };
-    __device__ static S unpack(const Payload &p) {
+    __device__ static S unpack(const Payload &p, float &ex, float &ey) {
+        ex = p.c.y;
+        ey = p.c.z;
         return S{p.a.x, p.a.y, p.a.z, p.a.w, p.b.x, p.b.y, p.b.z, p.b.w, p.c.x};
     }
 };
@@ -39,10 +41,25 @@ struct Px<double> {
     struct S {
         double mx, my, ca, cb, cc, alpha, r, g, b;
     };
-    __device__ static S unpack(const Payload &p) {
+    __device__ static S unpack(const Payload &p, float &ex, float &ey) {
+        ex = (float)p.e.y;
+        ey = (float)p.f.x;
         return S{p.a.x, p.a.y, p.b.x, p.b.y, p.c.x, p.c.y, p.d.x, p.d.y, p.e.x};
     }
 };
+
+// Pixel of thread t in a tile: 16x16 tiles give each warp an 8x4 block (so the
+// per-warp culling box is square-ish); other tile sizes are row-major.
+__device__ __forceinline__ void tile_pixel(int ts, int t, int &dx, int &dy) {
+    if (ts == 16) {
+        const int w = t >> 5, l = t & 31;
+        dx = (w & 1) * 8 + (l & 7);
+        dy = (w >> 1) * 4 + (l >> 3);
+    } else {
+        dx = t % ts;
+        dy = t / ts;
+    }
+}
 
 __device__ __forceinline__ float splat_exp(float x, const unsigned long long *tab) {
     return expf_glibc(x, tab);
@@ -56,16 +73,46 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
                             int32_t *__restrict__ last_contrib) {
     using S = typename Px<Real>::S;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nb = blockDim.x;
     S *sp = reinterpret_cast<S *>(smem_raw);
+    unsigned *smask = reinterpret_cast<unsigned *>(sp + nb);   // warps each splat can touch
     __shared__ unsigned long long s_tab[32];
+    __shared__ float4 s_wbox[32];                             // pixel-centre box per warp
     if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
 
     const int ts = vp.tile_size;
     const int tile = blockIdx.x;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    const int px = tx * ts + (int)threadIdx.x % ts;
-    const int py = ty * ts + (int)threadIdx.x / ts;
+    int ox, oy;
+    tile_pixel(ts, threadIdx.x, ox, oy);
+    const int px = tx * ts + ox;
+    const int py = ty * ts + oy;
     const bool inside = px < vp.iw && py < vp.ih;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = (nb + 31) >> 5;
+    const int wlanes = min(32, nb - warp * 32);
+    const unsigned wmask = wlanes == 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
+    if (threadIdx.x < nwarps) {   // pixel-centre box of warp w, clipped to the image
+        const int w = threadIdx.x;
+        int x0, x1, y0, y1;
+        if (ts == 16) {
+            x0 = (w & 1) * 8;
+            x1 = x0 + 7;
+            y0 = (w >> 1) * 4;
+            y1 = y0 + 3;
+        } else {
+            const int t0 = w * 32, t1 = min(nb, t0 + 32) - 1;
+            y0 = t0 / ts;
+            y1 = t1 / ts;
+            x0 = y0 == y1 ? t0 % ts : 0;
+            x1 = y0 == y1 ? t1 % ts : ts - 1;
+        }
+        x0 += tx * ts;
+        x1 = min(x1 + tx * ts, vp.iw - 1);
+        y0 += ty * ts;
+        y1 = min(y1 + ty * ts, vp.ih - 1);
+        s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
+                                           : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
+    }
     const int64_t lo = starts[tile], hi = starts[tile + 1];
     const Real fx = (Real)px, fy = (Real)py;
     const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
@@ -73,32 +120,53 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
     Real T = one, ar = 0, ag = 0, ab = 0, aa = 0;
     int last = 0;
     bool done = !inside;
-    const int nb = blockDim.x;
     for (int64_t b0 = lo; b0 < hi; b0 += nb) {
-        __syncthreads();   // previous batch fully consumed (and s_tab ready)
+        __syncthreads();   // previous batch consumed; s_tab / s_wbox ready
         const int64_t e = b0 + threadIdx.x;
-        if (e < hi) sp[threadIdx.x] = Px<Real>::unpack(payload[vals[e]]);
+        if (e < hi) {
+            float ex, ey;
+            const S s = Px<Real>::unpack(payload[vals[e]], ex, ey);
+            sp[threadIdx.x] = s;
+            const float mx = (float)s.mx, my = (float)s.my;
+            unsigned m = 0;
+            for (int w = 0; w < nwarps; ++w) {
+                const float4 bx = s_wbox[w];
+                if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w)
+                    m |= 1u << w;
+            }
+            smask[threadIdx.x] = m;
+        }
         __syncthreads();
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                const S s = sp[j];
-                const Real dx = fx - s.mx;
-                const Real dy = fy - s.my;
-                const Real pw = half * (s.ca * dx * dx + s.cc * dy * dy) - s.cb * dx * dy;
-                if (pw > (Real)0 || pw < skip_lo) continue;
-                const Real ai = s.alpha * splat_exp(pw, s_tab);
-                if (ai < floor_a) continue;
-                const Real w = ai * T;
-                ar = ar + s.r * w;
-                ag = ag + s.g * w;
-                ab = ab + s.b * w;
-                aa = aa + w;
-                T = T * (one - ai);
-                last = (int)(b0 - lo) + j + 1;
-                if (T < t_stop) {
-                    done = true;
-                    break;
+        if (!__all_sync(wmask, done)) {
+            for (int c0 = 0; c0 < cnt; c0 += 32) {
+                // ballot over the splats c0..c0+31 (one per lane, any warp width)
+                unsigned hits = 0;
+                for (int k = 0; k < 32; k += wlanes) {
+                    const int jl = c0 + k + lane;
+                    const unsigned b = __ballot_sync(
+                        wmask, lane + k < 32 && jl < cnt && ((smask[jl] >> warp) & 1u));
+                    hits |= b << k;
+                }
+                while (hits) {
+                    const int j = c0 + __ffs(hits) - 1;
+                    hits &= hits - 1;
+                    if (done) continue;
+                    const S s = sp[j];
+                    const Real dx = fx - s.mx;
+                    const Real dy = fy - s.my;
+                    const Real pw = half * (s.ca * dx * dx + s.cc * dy * dy) - s.cb * dx * dy;
+                    if (pw > (Real)0 || pw < skip_lo) continue;
+                    const Real ai = s.alpha * splat_exp(pw, s_tab);
+                    if (ai < floor_a) continue;
+                    const Real w = ai * T;
+                    ar = ar + s.r * w;
+                    ag = ag + s.g * w;
+                    ab = ab + s.b * w;
+                    aa = aa + w;
+                    T = T * (one - ai);
+                    last = (int)(b0 - lo) + j + 1;
+                    if (T < t_stop) done = true;
                 }
             }
         }
@@ -112,8 +180,8 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
             reinterpret_cast<double2 *>(image)[2 * p] = make_double2(ar, ag);
             reinterpret_cast<double2 *>(image)[2 * p + 1] = make_double2(ab, aa);
         }
-        final_t[p] = T;
-        last_contrib[p] = last;
+        if (final_t) final_t[p] = T;
+        if (last_contrib) last_contrib[p] = last;
     }
 }
 
@@ -123,11 +191,14 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
                                const Real *alphas, typename Px<Real>::Payload *out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
+    float ex, ey;
+    cull_extents((double)conics[3 * i], (double)conics[3 * i + 1], (double)conics[3 * i + 2],
+                 sizeof(Real) == 4 ? 0x1p-23 : 0x1p-52, ex, ey);
     if constexpr (sizeof(Real) == 4) {
         PayloadF32 p;
         p.a = make_float4(means2d[2 * i], means2d[2 * i + 1], conics[3 * i], conics[3 * i + 1]);
         p.b = make_float4(conics[3 * i + 2], alphas[i], colors[3 * i], colors[3 * i + 1]);
-        p.c = make_float4(colors[3 * i + 2], 0.f, 0.f, 0.f);
+        p.c = make_float4(colors[3 * i + 2], ex, ey, 0.f);
         out[i] = p;
     } else {
         PayloadF64 p;
@@ -135,7 +206,8 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
         p.b = make_double2(conics[3 * i], conics[3 * i + 1]);
         p.c = make_double2(conics[3 * i + 2], alphas[i]);
         p.d = make_double2(colors[3 * i], colors[3 * i + 1]);
-        p.e = make_double2(colors[3 * i + 2], 0.0);
+        p.e = make_double2(colors[3 * i + 2], (double)ex);
+        p.f = make_double2((double)ey, 0.0);
         out[i] = p;
     }
 }
@@ -236,13 +308,21 @@ int launch_composite(const ViewParams &vp, const void *payload, const unsigned *
     const int threads = vp.tile_size * vp.tile_size;
     const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
     if (grid == 0) return G6R_OK;
+    static bool attrs_set = false;   // >48 KB dynamic smem for 32x32 f64 tiles
+    if (!attrs_set) {
+        cudaFuncSetAttribute(k_composite<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             1024 * (int)(sizeof(Px<double>::S) + 4));
+        cudaFuncSetAttribute(k_composite<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             1024 * (int)(sizeof(Px<float>::S) + 4));
+        attrs_set = true;
+    }
     if (vp.precision) {
-        const size_t smem = threads * sizeof(Px<double>::S);
+        const size_t smem = threads * (sizeof(Px<double>::S) + sizeof(unsigned));
         k_composite<double><<<grid, threads, smem, st>>>(vp, (const PayloadF64 *)payload, entry_vals,
                                                          tile_starts, (double *)image,
                                                          (double *)final_t, last_contrib);
     } else {
-        const size_t smem = threads * sizeof(Px<float>::S);
+        const size_t smem = threads * (sizeof(Px<float>::S) + sizeof(unsigned));
         k_composite<float><<<grid, threads, smem, st>>>(vp, (const PayloadF32 *)payload, entry_vals,
                                                         tile_starts, (float *)image,
                                                         (float *)final_t, last_contrib);

@@ -346,18 +346,24 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (kept) {
         const long long m = m_base + lm;
         if (kF64) {
+            float ex, ey;
+            cull_extents(o.ca, o.cb, o.cc, 0x1p-52, ex, ey);
             PayloadF64 p;
             p.a = make_double2(o.u, o.v);
             p.b = make_double2(o.ca, o.cb);
             p.c = make_double2(o.cc, o.alpha);
             p.d = make_double2(o.r, o.g);
-            p.e = make_double2(o.b, 0.0);
+            p.e = make_double2(o.b, (double)ex);
+            p.f = make_double2((double)ey, 0.0);
             reinterpret_cast<PayloadF64 *>(ws.payload)[m] = p;
         } else {
+            const float fa = (float)o.ca, fb = (float)o.cb, fc = (float)o.cc;
+            float ex, ey;
+            cull_extents(fa, fb, fc, 0x1p-23, ex, ey);
             PayloadF32 p;
-            p.a = make_float4((float)o.u, (float)o.v, (float)o.ca, (float)o.cb);
-            p.b = make_float4((float)o.cc, (float)o.alpha, (float)o.r, (float)o.g);
-            p.c = make_float4((float)o.b, 0.f, 0.f, 0.f);
+            p.a = make_float4((float)o.u, (float)o.v, fa, fb);
+            p.b = make_float4(fc, (float)o.alpha, (float)o.r, (float)o.g);
+            p.c = make_float4((float)o.b, ex, ey, 0.f);
             reinterpret_cast<PayloadF32 *>(ws.payload)[m] = p;
         }
         if (so.gids) so.gids[m] = i;

@@ -506,9 +506,13 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
     return _launch(prep, bits, camera, config, False, int(capacity or prep.entry_hint))
 
 
+DEFAULT_CONCURRENCY = 4
+
+
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
-                 capacity: int | None = None, out=None, profiler=None):
-    """Render ``cameras`` (same size) back to back on the current stream.
+                 capacity: int | None = None, out=None, profiler=None,
+                 concurrency: int = DEFAULT_CONCURRENCY):
+    """Render ``cameras`` (same size) with up to ``concurrency`` views in flight.
 
     Returns ``(images, counters)``: ``images`` (V,H,W,4) on the device,
     ``counters`` (V,16) int64.  No synchronisation; a view with
@@ -519,24 +523,26 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     cams = list(cameras)
     V = len(cams)
     H, W = int(cams[0].height), int(cams[0].width)
+    if any(int(c.height) != H or int(c.width) != W for c in cams):
+        raise InvalidParameterError("render_views needs cameras of one image size")
     dt = torch.float32 if config.precision == "f32" else torch.float64
     dev = prep.device
     images = out if out is not None else torch.empty((V, H, W, 4), dtype=dt, device=dev)
-    final_t = torch.empty((H, W), dtype=dt, device=dev)
-    last = torch.empty((H, W), dtype=torch.int32, device=dev)
     counters = torch.empty((V, nat.NCOUNTERS), dtype=torch.int64, device=dev)
     cap = int(capacity or prep.entry_hint)
+    slots = max(1, min(int(concurrency), 8, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
-    ws, nbytes = _workspace(prep.n, tx * ty, cap, cfg.precision, dev)
+    per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
+    ws = torch.empty(max(per * slots, 256), dtype=torch.uint8, device=dev)
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
-    frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr(), final_t.data_ptr(), last.data_ptr(),
-                                         counters[v].data_ptr(), 0, 0) for v in range(V)])
+    frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr(), 0, 0, counters[v].data_ptr(), 0, 0)
+                               for v in range(V)])
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
-                                          _ptr(ws), nbytes, cap, frames,
+                                          _ptr(ws), per * slots, cap, frames, slots,
                                           profiler.handle if profiler is not None else None,
                                           _stream_handle()))
-    images._g6r_keepalive = (ws, final_t, last)
+    images._g6r_keepalive = ws
     return images, counters
 
 

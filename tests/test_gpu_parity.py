@@ -127,7 +127,8 @@ def test_projection_bitwise_given_oracle_prep(oracle, seed, n):
     np.testing.assert_array_equal(got.gids, want.gids)
     for f in ("means2d", "conics", "colors", "depths", "radii"):
         np.testing.assert_array_equal(getattr(got, f), getattr(want, f), err_msg=f)
-    assert ulp_diff(got.alphas, want.alphas).max() <= 1
+    # exp(-q/2): CUDA exp and numpy's SIMD exp are each within 1 ulp of exact
+    assert ulp_diff(got.alphas, want.alphas).max() <= 2
     np.testing.assert_array_equal(np.bincount(want.stage, minlength=6)[1:6],
                                   [stats.n_view_degenerate, stats.n_alpha_culled,
                                    stats.n_depth_culled, stats.n_projection_culled,
