@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--gaussians", type=int, default=N_GAUSS)
     ap.add_argument("--e2e-views", type=int, default=60)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--concurrency", type=int, default=4,
+                    help="views in flight per GPU (1 = serial; per-stage times are then exact)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -277,7 +279,8 @@ def run_b200(args):
     images = torch.empty((len(cams), args.size, args.size, 4), dtype=torch.float32, device=dev)
     prof = nat.Profiler(len(cams))
     for _ in range(2):
-        raster.render_views(scene, cams[:4], config=cfg, capacity=cap, out=images[:4])
+        raster.render_views(scene, cams[:4], config=cfg, capacity=cap, out=images[:4],
+                            concurrency=args.concurrency)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -287,7 +290,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     ev0.record()
     _, counters = raster.render_views(scene, cams, config=cfg, capacity=cap, out=images,
-                                      profiler=prof)
+                                      profiler=prof, concurrency=args.concurrency)
     ev1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()

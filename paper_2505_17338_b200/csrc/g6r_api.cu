@@ -49,7 +49,7 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     L.internal = o;
     o = align_up(o + kNumInternal * sizeof(int64_t));
     L.hist = o;
-    o = align_up(o + kMaxPasses * 256 * sizeof(unsigned));
+    o = align_up(o + kMaxPasses * kBins * sizeof(unsigned));
     L.proj = o;
     const int64_t nblk = ceil_div(n > 0 ? n : 1, kBlock);
     o = align_up(o + 4 * nblk * sizeof(unsigned long long));
@@ -68,7 +68,7 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + (size_t)cap * 4);
     L.sort_tiles_cap = ceil_div(cap > 0 ? cap : 1, kSortTile);
     L.sort_status = o;
-    o = align_up(o + (size_t)kMaxPasses * L.sort_tiles_cap * 256 * sizeof(unsigned));
+    o = align_up(o + (size_t)kMaxPasses * L.sort_tiles_cap * kBins * sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -203,14 +203,13 @@ static int render_one(const g6r_scene *scene, uint32_t mask, const g6r_camera *c
     int rc = launch_project(*scene, mask, vp, ws, fr->counters, splats, true, st);
     if (rc) return cuda_check("project");
     prof_mark(prof, 1, st);
-    int final_buf = 0;
-    rc = launch_sort(vp, ws, fr->counters, &final_buf, st);
+    rc = launch_sort(vp, ws, fr->counters, st);
     if (rc) return cuda_check("sort");
     prof_mark(prof, 2, st);
-    rc = launch_ranges(vp, ws, fr->counters, final_buf, fr->tile_starts, fr->entry_splat, st);
+    rc = launch_ranges(vp, ws, fr->counters, fr->tile_starts, fr->entry_splat, st);
     if (rc) return cuda_check("ranges");
     prof_mark(prof, 3, st);
-    rc = launch_composite(vp, ws.payload, ws.vals[final_buf], ws.tile_starts, fr->image, fr->final_t,
+    rc = launch_composite(vp, ws.payload, ws.vals[0], ws.vals[1], ws.internal, ws.tile_starts, fr->image, fr->final_t,
                           fr->last_contrib, st);
     if (rc) return cuda_check("composite");
     prof_mark(prof, 4, st);
@@ -415,8 +414,8 @@ int g6r_bin(int64_t m, const double *means2d, const int32_t *radii, const double
         return cuda_check("memset");
     if (launch_duplicate(m, means2d, radii, depths, vp, ws, counters, st)) return cuda_check("duplicate");
     int final_buf = 0;
-    if (launch_sort(vp, ws, counters, &final_buf, st)) return cuda_check("sort");
-    if (launch_ranges(vp, ws, counters, final_buf, tile_starts, entry_splat, st)) return cuda_check("ranges");
+    if (launch_sort(vp, ws, counters, st)) return cuda_check("sort");
+    if (launch_ranges(vp, ws, counters, tile_starts, entry_splat, st)) return cuda_check("ranges");
     return G6R_OK;
 }
 
@@ -444,7 +443,7 @@ int g6r_composite(int64_t m, int32_t precision, const void *means2d, const void 
     vp.tiles_x = tiles_x;
     vp.tiles_y = tiles_y;
     vp.precision = precision;
-    if (launch_composite(vp, ws.payload, reinterpret_cast<const unsigned *>(entry_splat), tile_starts,
+    if (launch_composite(vp, ws.payload, reinterpret_cast<const unsigned *>(entry_splat), nullptr, nullptr, tile_starts,
                          image, final_t, last_contrib, st))
         return cuda_check("composite");
     return G6R_OK;

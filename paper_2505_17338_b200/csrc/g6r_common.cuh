@@ -19,12 +19,30 @@ constexpr int kSortItems = 16;       // keys per thread in a onesweep tile
 constexpr int kSortTile = kBlock * kSortItems;   // 4096 keys per tile
 constexpr double kMinAlpha = 1.0 / 255.0;        // raster.py:47
 
-// internal counter slots (int64) at the head of every workspace
+constexpr int kRadixBits = 9;                    // LSD digit width
+constexpr int kBins = 1 << kRadixBits;
+
+// internal counter slots (int64) at the head of every workspace (zeroed per view)
 enum {
     kTicketProject = 0,
     kTicketSortBase = 1,   // 1..8: one per radix pass
+    kDepthMinInv = 10,     // ~min f32 depth bits of the drawn splats (atomicMax of ~bits)
+    kDepthMax = 11,        // max f32 depth bits
+    kSortPasses = 12,      // radix passes actually needed (decided on the device)
     kNumInternal = 16
 };
+
+// Which ping-pong buffer holds the sorted entries after the radix passes.
+__device__ __forceinline__ int sorted_buffer(const long long *internal) {
+    return (int)(internal[kSortPasses] & 1);
+}
+
+// Fold a CTA's depth-bit extrema (max of ~bits, max of bits) into the view's.
+__device__ __forceinline__ void note_depth_extrema(long long *internal, unsigned lo_inv, unsigned hi) {
+    atomicMax(reinterpret_cast<unsigned long long *>(&internal[kDepthMinInv]),
+              (unsigned long long)lo_inv);
+    atomicMax(reinterpret_cast<unsigned long long *>(&internal[kDepthMax]), (unsigned long long)hi);
+}
 
 // Per-splat compositing payload (f32): (mx, my, conic_a, conic_b),
 // (conic_c, alpha, r, g), (b, cull_x, cull_y, -).  48 bytes, 16-byte aligned.

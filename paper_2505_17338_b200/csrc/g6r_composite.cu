@@ -68,7 +68,8 @@ __device__ __forceinline__ double splat_exp(double x, const unsigned long long *
 
 template <typename Real>
 __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__restrict__ payload,
-                            const unsigned *__restrict__ vals, const int64_t *__restrict__ starts,
+                            const unsigned *vals0, const unsigned *vals1, const long long *sel,
+                            const int64_t *__restrict__ starts,
                             Real *__restrict__ image, Real *__restrict__ final_t,
                             int32_t *__restrict__ last_contrib) {
     using S = typename Px<Real>::S;
@@ -113,6 +114,7 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
         s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
                                            : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
     }
+    const unsigned *__restrict__ vals = (sel && sorted_buffer(sel)) ? vals1 : vals0;
     const int64_t lo = starts[tile], hi = starts[tile + 1];
     const Real fx = (Real)px, fy = (Real)py;
     const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
@@ -302,9 +304,9 @@ int launch_pack_payload(int64_t m, int precision, const void *means2d, const voi
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
-int launch_composite(const ViewParams &vp, const void *payload, const unsigned *entry_vals,
-                     const int64_t *tile_starts, void *image, void *final_t, int32_t *last_contrib,
-                     cudaStream_t st) {
+int launch_composite(const ViewParams &vp, const void *payload, const unsigned *vals0,
+                     const unsigned *vals1, const long long *sel, const int64_t *tile_starts,
+                     void *image, void *final_t, int32_t *last_contrib, cudaStream_t st) {
     const int threads = vp.tile_size * vp.tile_size;
     const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
     if (grid == 0) return G6R_OK;
@@ -318,12 +320,12 @@ int launch_composite(const ViewParams &vp, const void *payload, const unsigned *
     }
     if (vp.precision) {
         const size_t smem = threads * (sizeof(Px<double>::S) + sizeof(unsigned));
-        k_composite<double><<<grid, threads, smem, st>>>(vp, (const PayloadF64 *)payload, entry_vals,
+        k_composite<double><<<grid, threads, smem, st>>>(vp, (const PayloadF64 *)payload, vals0, vals1, sel,
                                                          tile_starts, (double *)image,
                                                          (double *)final_t, last_contrib);
     } else {
         const size_t smem = threads * (sizeof(Px<float>::S) + sizeof(unsigned));
-        k_composite<float><<<grid, threads, smem, st>>>(vp, (const PayloadF32 *)payload, entry_vals,
+        k_composite<float><<<grid, threads, smem, st>>>(vp, (const PayloadF32 *)payload, vals0, vals1, sel,
                                                         tile_starts, (float *)image,
                                                         (float *)final_t, last_contrib);
     }

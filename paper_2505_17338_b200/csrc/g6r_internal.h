@@ -15,8 +15,8 @@ struct Workspace {
     void *payload;                  // n compositing payloads (f32 or f64)
     unsigned long long *keys[2];    // entry keys, ping-pong
     unsigned *vals[2];              // entry values (splat index), ping-pong
-    unsigned *hist;                 // kMaxPasses x 256 digit counts
-    unsigned *sort_status;          // kMaxPasses x tiles_cap x 256 lookback words
+    unsigned *hist;                 // kMaxPasses x kBins digit counts
+    unsigned *sort_status;          // kMaxPasses x tiles_cap x kBins lookback words
     int64_t *tile_starts;           // T+1 (internal copy)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
@@ -48,16 +48,16 @@ int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, con
                      const ViewParams &vp, const Workspace &ws, int64_t *counters, cudaStream_t st);
 // radix sort of ws.keys[0]/vals[0] (E read from counters); *final_buf receives
 // the index (0/1) of the buffer holding the sorted result.
-int launch_sort(const ViewParams &vp, const Workspace &ws, const int64_t *counters, int *final_buf,
-                cudaStream_t st);
+int launch_sort(const ViewParams &vp, const Workspace &ws, const int64_t *counters, cudaStream_t st);
 // per-tile ranges into ws.tile_starts (+ optional copies of starts / entry_splat)
-int launch_ranges(const ViewParams &vp, const Workspace &ws, const int64_t *counters, int buf,
+int launch_ranges(const ViewParams &vp, const Workspace &ws, const int64_t *counters,
                   int64_t *tile_starts_out, int32_t *entry_splat_out, cudaStream_t st);
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st);
 int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
                         const void *colors, const void *alphas, void *payload, cudaStream_t st);
-int launch_composite(const ViewParams &vp, const void *payload, const unsigned *entry_vals,
-                     const int64_t *tile_starts, void *image, void *final_t,
+// entry values: vals0, or (sel != NULL) the sorted ping-pong buffer sel picks
+int launch_composite(const ViewParams &vp, const void *payload, const unsigned *vals0,
+                     const unsigned *vals1, const long long *sel, const int64_t *tile_starts, void *image, void *final_t,
                      int32_t *last_contrib, cudaStream_t st);
 int launch_composite_backward(int64_t m, const double *means2d, const double *conics,
                               const double *colors, const double *alphas,

@@ -148,8 +148,18 @@ __device__ __forceinline__ void tile_rect(double u, double v, int32_t rx, int32_
     hy = (int)(d - c + 1);
 }
 
-constexpr unsigned long long kFlagReady = 1ull << 63;
-constexpr unsigned long long kValMask = kFlagReady - 1;
+// Look-back status: one 64-bit word per CTA, [63:62] flag (1 aggregate,
+// 2 inclusive prefix), [61:32] splat count, [31:0] entry count (saturating).
+// A single volatile 64-bit store publishes flag and both sums together, so no
+// memory fence is needed (a __threadfence here is MEMBAR.SC + L1 invalidate).
+constexpr unsigned long long kAggFlag = 1ull << 62, kIncFlag = 2ull << 62;
+constexpr unsigned long long kECap = 0xffffffffull;
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, long long m,
+                                                          long long e) {
+    const unsigned long long ec = e < (long long)kECap ? (unsigned long long)e : kECap;
+    return flag | ((unsigned long long)m << 32) | ec;
+}
 
 // Decoupled look-back over CTAs carrying two sums (splats, entries).
 // Returns this CTA's exclusive prefix (pm, pe) in shared memory.
@@ -158,51 +168,49 @@ __device__ __forceinline__ void lookback2(int64_t tile, long long bm, long long 
                                           long long *s_pe) {
     const int lane = threadIdx.x & 31;
     if (threadIdx.x >= 32) return;
+    unsigned long long *status = ws.proj_inc_m;
     if (tile == 0) {
         if (lane == 0) {
-            st_volatile_u64(ws.proj_inc_e, (unsigned long long)be);
-            __threadfence();
-            st_volatile_u64(ws.proj_inc_m, kFlagReady | (unsigned long long)bm);
+            st_volatile_u64(status, pack_status(kIncFlag, bm, be));
             *s_pm = 0;
             *s_pe = 0;
         }
         return;
     }
-    if (lane == 0) {
-        st_volatile_u64(ws.proj_agg_e + tile, (unsigned long long)be);
-        __threadfence();
-        st_volatile_u64(ws.proj_agg_m + tile, kFlagReady | (unsigned long long)bm);
-    }
+    if (lane == 0) st_volatile_u64(status + tile, pack_status(kAggFlag, bm, be));
+    // Each probe covers 32 x kLB predecessors (lane l owns distances
+    // l*kLB+1 .. l*kLB+kLB).  The inclusive-prefix frontier advances by the
+    // probe width per L2 round trip, so a narrow probe, not the work, would
+    // bound a launch of thousands of short CTAs.
+    constexpr int kLB = 8;
     long long pm = 0, pe = 0;
     int64_t j0 = tile - 1;
     while (true) {
-        const int64_t j = j0 - lane;
-        unsigned long long mw = kFlagReady, ev = 0;
-        bool inc = true;
-        if (j >= 0) {
-            while (true) {
-                unsigned long long w = ld_volatile_u64(ws.proj_inc_m + j);
-                if (w) {
-                    __threadfence();
-                    ev = ld_volatile_u64(ws.proj_inc_e + j);
-                    mw = w;
-                    inc = true;
-                    break;
-                }
-                w = ld_volatile_u64(ws.proj_agg_m + j);
-                if (w) {
-                    __threadfence();
-                    ev = ld_volatile_u64(ws.proj_agg_e + j);
-                    mw = w;
-                    inc = false;
-                    break;
-                }
-            }
+        unsigned long long w[kLB];
+#pragma unroll
+        for (int k = 0; k < kLB; ++k) {
+            const int64_t j = j0 - lane * kLB - k;
+            w[k] = j >= 0 ? ld_volatile_u64(status + j) : kIncFlag;
         }
-        const unsigned inc_mask = __ballot_sync(0xffffffffu, inc);
+        int kfirst = kLB;
+#pragma unroll
+        for (int k = 0; k < kLB; ++k) {
+            const int64_t j = j0 - lane * kLB - k;
+            while (!(w[k] >> 62)) w[k] = ld_volatile_u64(status + j);
+        }
+#pragma unroll
+        for (int k = kLB - 1; k >= 0; --k)
+            if ((w[k] >> 62) == 2) kfirst = k;
+        long long cm = 0, ce = 0;
+#pragma unroll
+        for (int k = 0; k < kLB; ++k)
+            if (k <= kfirst) {
+                cm += (long long)((w[k] >> 32) & 0x3fffffffull);
+                ce += (long long)(w[k] & kECap);
+            }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, kfirst < kLB);
         const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
-        long long cm = lane <= first ? (long long)(mw & kValMask) : 0;
-        long long ce = lane <= first ? (long long)ev : 0;
+        if (lane > first) cm = ce = 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             cm += __shfl_xor_sync(0xffffffffu, cm, o);
@@ -211,12 +219,10 @@ __device__ __forceinline__ void lookback2(int64_t tile, long long bm, long long 
         pm += cm;
         pe += ce;
         if (inc_mask) break;
-        j0 -= 32;
+        j0 -= 32 * kLB;
     }
     if (lane == 0) {
-        st_volatile_u64(ws.proj_inc_e + tile, (unsigned long long)(pe + be));
-        __threadfence();
-        st_volatile_u64(ws.proj_inc_m + tile, kFlagReady | (unsigned long long)(pm + bm));
+        st_volatile_u64(status + tile, pack_status(kIncFlag, pm + bm, pe + be));
         *s_pm = pm;
         *s_pe = pe;
     }
@@ -290,8 +296,10 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     __shared__ unsigned s_fate[6];
     __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
     __shared__ unsigned s_db[kBlock];
+    __shared__ unsigned s_dext[2];   // block max of ~depth_bits and of depth_bits
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
     if (threadIdx.x < 6) s_fate[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t n = scene.n;
@@ -304,10 +312,11 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (i < n) {
         const unsigned fl = scene.flags[i];
         if (((mask >> (fl & 15u)) & 1u) && !(fl & G6R_FLAG_DEGENERATE)) {
+            // all 22 column packets issued at once: one HBM round trip per Gaussian
             double r[G6R_REC_DOUBLES];
 #pragma unroll
-            for (int c = 0; c < 11; ++c) {   // mu_p, mu_d, adjust, precision_dd
-                const double2 q = __ldg(&rec[c * n + i]);
+            for (int c = 0; c < G6R_REC_COLUMNS; ++c) {
+                const double2 q = __ldcs(&rec[c * n + i]);   // streamed once per view
                 r[2 * c] = q.x;
                 r[2 * c + 1] = q.y;
             }
@@ -315,22 +324,13 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
             st = slice_row(r + 0, r + 3, r + 6, r + 15, vp.pos[0], vp.pos[1], vp.pos[2], view, madj,
                            quad);
             if (st == 0) {
-                const double2 q = __ldg(&rec[21 * n + i]);   // opacity, w_norm
-                const double w = exp(-0.5 * quad) * q.y;
-                double alpha = q.x * w;
+                const double w = exp(-0.5 * quad) * r[43];   // opacity modulation (raster.py:259-261)
+                double alpha = r[42] * w;
                 alpha = alpha > vp.alpha_max ? vp.alpha_max : alpha;   // np.minimum (NaN stays)
                 o.alpha = alpha;
                 if (!(alpha >= kMinAlpha)) st = 2;
             }
-            if (st == 0) {
-#pragma unroll
-                for (int c = 11; c < 21; ++c) {   // sigma_prime (tail of col 10 already read), sh
-                    const double2 q = __ldg(&rec[c * n + i]);
-                    r[2 * c] = q.x;
-                    r[2 * c + 1] = q.y;
-                }
-                st = project_row(view, madj, r + 30, r + 21, vp, sh_c0, sh_c1, o);
-            }
+            if (st == 0) st = project_row(view, madj, r + 30, r + 21, vp, sh_c0, sh_c1, o);
             if (st == 0) tile_rect(o.u, o.v, o.rx, o.ry, vp, x0, y0, wx, hy);
         }
         if (so.stage) so.stage[i] = (uint8_t)st;
@@ -338,6 +338,15 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (st < 6) atomicAdd(&s_fate[st], 1u);
     const int kept = st == 0;
     const int cnt = kept ? wx * hy : 0;
+    {   // view depth-bit extrema for the radix key compression (g6r_sort.cu)
+        const unsigned db = kept ? __float_as_uint((float)o.depth) : 0u;
+        const unsigned hi = __reduce_max_sync(0xffffffffu, db);
+        const unsigned lo_inv = __reduce_max_sync(0xffffffffu, kept ? ~db : 0u);
+        if ((threadIdx.x & 31) == 0 && hi) {
+            atomicMax(&s_dext[0], lo_inv);
+            atomicMax(&s_dext[1], hi);
+        }
+    }
     int lm, le, bm, be;
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
     lookback2(tile, bm, be, ws, &s_pm, &s_pe);
@@ -397,6 +406,7 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (threadIdx.x < 6 && s_fate[threadIdx.x])
         atomicAdd((unsigned long long *)&counters[G6R_CNT_FATE + threadIdx.x],
                   (unsigned long long)s_fate[threadIdx.x]);
+    if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
     if (write_entries) {
         if (e_base + be <= ws.entry_capacity) {
             emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0],
@@ -420,7 +430,9 @@ k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__rest
     __shared__ long long s_pm, s_pe;
     __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
     __shared__ unsigned s_db[kBlock];
+    __shared__ unsigned s_dext[2];
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
+    if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t i = tile * kBlock + threadIdx.x;
@@ -428,6 +440,15 @@ k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__rest
     const int kept = i < m;
     if (kept) tile_rect(means2d[2 * i], means2d[2 * i + 1], radii[2 * i], radii[2 * i + 1], vp, x0, y0, wx, hy);
     const int cnt = kept ? wx * hy : 0;
+    {
+        const unsigned db = kept ? __float_as_uint((float)depths[i]) : 0u;
+        const unsigned hi = __reduce_max_sync(0xffffffffu, db);
+        const unsigned lo_inv = __reduce_max_sync(0xffffffffu, kept ? ~db : 0u);
+        if ((threadIdx.x & 31) == 0 && (hi | lo_inv)) {
+            atomicMax(&s_dext[0], lo_inv);
+            atomicMax(&s_dext[1], hi);
+        }
+    }
     int lm, le, bm, be;
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
     lookback2(tile, bm, be, ws, &s_pm, &s_pe);
@@ -440,6 +461,7 @@ k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__rest
         s_db[lm] = __float_as_uint((float)depths[i]);
     }
     __syncthreads();
+    if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
     const long long m_base = s_pm, e_base = s_pe;
     if (e_base + be <= ws.entry_capacity) {
         emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0], ws.vals[0]);

@@ -6,14 +6,24 @@
 // Stability reproduces the reference tie rule (equal keys keep splat order,
 // raster.py:22-24), so the output is bit-identical to the reference.
 //
-// Design: one histogram launch computes every pass's digit counts at once
-// (LSD digit counts do not depend on the order), then one "onesweep" launch
-// per 8-bit digit: each CTA ranks a 4096-key tile with warp match-any, gets
-// its global digit offsets by decoupled look-back over earlier tiles, and
-// scatters.  Tiles are claimed through an atomic ticket so a CTA only ever
-// waits on tiles already owned by running CTAs.  E is read on the device;
-// grids are sized from the capacity and idle CTAs exit, so there is no host
-// round trip between projection and compositing.
+// Key compression: depths are positive, so their f32 bit patterns order
+// monotonically; the projection records the view's min/max depth bits and the
+// sort ranks the order-preserving key' = tile << dbits | (depth_bits - dmin)
+// with dbits = bits(dmax - dmin).  At 512^2 with a 1M-Gaussian orbit view that
+// is ~10 + 24 bits: 4 passes of 9-bit digits instead of 6 passes of 8 bits.
+// The stored keys stay the original 64-bit keys (ranges read the tile from
+// them); digits are computed on the fly.  The pass count is decided on the
+// device; surplus pass launches exit at once and consumers read which
+// ping-pong buffer holds the result (sorted_buffer()).
+//
+// Each pass is reduce-then-scan over 4096-key tiles, with no inter-CTA waiting:
+//   upsweep    per-tile digit counts (warp match-any aggregated smem atomics)
+//              + global digit totals;
+//   colscan    exclusive scan of every digit column across tiles;
+//   downsweep  re-rank each tile (stable: warp-striped items, warps in order),
+//              scatter to global digit offset + column prefix + local rank.
+// (A decoupled look-back version was latency-bound: its inclusive-prefix
+// frontier advances one probe width per L2 round trip, ~30 us per pass.)
 #include <algorithm>
 
 #include "g6r_common.cuh"
@@ -21,82 +31,159 @@
 
 namespace g6r {
 
-constexpr unsigned kAgg = 1u << 30, kInc = 2u << 30, kCntMask = (1u << 30) - 1;
+constexpr int kWarps = kBlock / 32;
+constexpr int kDigitsPerThread = kBins / kBlock;   // 2
 
-int sort_passes(int tiles) {
+int tile_bits(int64_t tiles) {
     int tb = 0;
-    while ((1ll << tb) < (long long)tiles) ++tb;
-    return (32 + tb + 7) / 8;
+    while ((1ll << tb) < tiles) ++tb;
+    return tb;
 }
+
+int sort_passes(int tiles) {   // upper bound (full 32 depth bits)
+    return (32 + tile_bits(tiles) + kRadixBits - 1) / kRadixBits;
+}
+
+struct SortParams {
+    int64_t cap;
+    int tbits;
+};
 
 __device__ __forceinline__ bool entries_valid(const int64_t *counters, int64_t cap, int64_t &e) {
     e = counters[G6R_CNT_ENTRIES];
     return !counters[G6R_CNT_OVERFLOW] && e <= cap;
 }
 
+// (dmin, dbits, passes) of this view from the projection's depth-bit extrema.
+__device__ __forceinline__ void view_key_shape(const long long *internal, int tbits, unsigned &dmin,
+                                               int &dbits, int &passes) {
+    const unsigned lo = ~(unsigned)internal[kDepthMinInv];
+    const unsigned hi = (unsigned)internal[kDepthMax];
+    const unsigned span = hi >= lo ? hi - lo : 0u;
+    dmin = hi >= lo ? lo : 0u;
+    dbits = span ? 32 - __clz(span) : 0;
+    passes = (tbits + dbits + kRadixBits - 1) / kRadixBits;
+}
+
+__device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dmin, int dbits,
+                                             int shift) {
+    const unsigned long long k2 =
+        ((key >> 32) << dbits) | (unsigned long long)((unsigned)key - dmin);
+    return (unsigned)(k2 >> shift) & (kBins - 1);
+}
+
 __global__ void __launch_bounds__(kBlock)
-k_sort_hist(const unsigned long long *__restrict__ keys, const int64_t *counters, int64_t cap,
-            int passes, unsigned *__restrict__ hist, unsigned *__restrict__ status,
-            int64_t tiles_cap) {
-    __shared__ unsigned h[kMaxPasses][256];
+k_upsweep(const unsigned long long *__restrict__ keys, const int64_t *counters, SortParams sp,
+          long long *internal, int pass, unsigned *__restrict__ counts,
+          unsigned *__restrict__ totals) {
+    __shared__ unsigned h[kBins];
     int64_t e;
-    if (!entries_valid(counters, cap, e)) return;
+    if (!entries_valid(counters, sp.cap, e)) return;
+    unsigned dmin;
+    int dbits, passes;
+    view_key_shape(internal, sp.tbits, dmin, dbits, passes);
+    if (pass == 0 && blockIdx.x == 0 && threadIdx.x == 0) internal[kSortPasses] = passes;
+    if (pass >= passes) return;
     const int64_t ntiles = ceil_div(e, kSortTile);
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-    for (int p = 0; p < passes; ++p)
-        for (int64_t k = gtid; k < ntiles * 256; k += gsz) status[p * tiles_cap * 256 + k] = 0u;
-    for (int k = threadIdx.x; k < kMaxPasses * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
-    __syncthreads();
+    const int shift = kRadixBits * pass;
     const int lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < e; base += gsz) {
-        const int64_t idx = base + threadIdx.x;
-        const bool valid = idx < e;
-        const unsigned long long key = valid ? keys[idx] : 0ull;
-        for (int p = 0; p < passes; ++p) {
-            const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 255ull) : 256u;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int k = threadIdx.x; k < kBins; k += kBlock) h[k] = 0u;
+        __syncthreads();
+        const int64_t base = tile * kSortTile;
+#pragma unroll 4
+        for (int k = 0; k < kSortItems; ++k) {
+            const int64_t idx = base + k * kBlock + threadIdx.x;
+            const unsigned d = idx < e ? digit_of(keys[idx], dmin, dbits, shift) : (unsigned)kBins;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&h[p][d], (unsigned)__popc(peers));
+            if (d < (unsigned)kBins && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
         }
+        __syncthreads();
+        for (int d = threadIdx.x; d < kBins; d += kBlock) {
+            const unsigned c = h[d];
+            counts[tile * kBins + d] = c;
+            if (c) atomicAdd(&totals[d], c);
+        }
+        __syncthreads();
     }
+}
+
+// Exclusive scan of each digit column across tiles.  CTA c owns 32 digit
+// columns (lane = digit); its 8 warps each sum a contiguous chunk of tiles,
+// the chunk sums are scanned in smem, then each warp rewrites its chunk.
+__global__ void __launch_bounds__(kBlock)
+k_colscan(const int64_t *counters, SortParams sp, const long long *internal, int pass,
+          unsigned *__restrict__ counts) {
+    __shared__ unsigned s_sum[kWarps][32];
+    int64_t e;
+    if (!entries_valid(counters, sp.cap, e)) return;
+    unsigned dmin;
+    int dbits, passes;
+    view_key_shape(internal, sp.tbits, dmin, dbits, passes);
+    if (pass >= passes) return;
+    const int64_t ntiles = ceil_div(e, kSortTile);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int d = blockIdx.x * 32 + lane;
+    const int64_t per = ceil_div(ntiles, kWarps);
+    const int64_t t0 = warp * per, t1 = std::min<int64_t>(ntiles, t0 + per);
+    constexpr int U = 8;   // independent loads in flight per lane
+    unsigned s = 0;
+    for (int64_t t = t0; t < t1; t += U) {
+        unsigned c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = t + u < t1 ? counts[(t + u) * kBins + d] : 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += c[u];
+    }
+    s_sum[warp][lane] = s;
     __syncthreads();
-    for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) {
-        const unsigned v = (&h[0][0])[k];
-        if (v) atomicAdd(&hist[k], v);
+    unsigned run = 0;
+    for (int w = 0; w < warp; ++w) run += s_sum[w][lane];
+    for (int64_t t = t0; t < t1; t += U) {
+        unsigned c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = t + u < t1 ? counts[(t + u) * kBins + d] : 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (t + u < t1) counts[(t + u) * kBins + d] = run;
+            run += c[u];
+        }
     }
 }
 
 __global__ void __launch_bounds__(kBlock)
-k_onesweep(const unsigned long long *__restrict__ kin, const unsigned *__restrict__ vin,
-           unsigned long long *__restrict__ kout, unsigned *__restrict__ vout,
-           const int64_t *counters, int64_t cap, int shift, const unsigned *__restrict__ hist_p,
-           unsigned *status_p, unsigned long long *ticket) {
-    __shared__ unsigned s_goff[256];
-    __shared__ unsigned s_wh[kBlock / 32][256];
-    __shared__ unsigned s_base[256];
-    __shared__ unsigned s_scan[kBlock / 32];
-    __shared__ int64_t s_tile;
+k_downsweep(const unsigned long long *__restrict__ kin, const unsigned *__restrict__ vin,
+            unsigned long long *__restrict__ kout, unsigned *__restrict__ vout,
+            const int64_t *counters, SortParams sp, const long long *internal, int pass,
+            const unsigned *__restrict__ counts, const unsigned *__restrict__ totals) {
+    __shared__ unsigned s_goff[kBins];
+    __shared__ unsigned s_wh[kWarps][kBins];
+    __shared__ unsigned s_scan[kWarps];
     int64_t e;
-    if (!entries_valid(counters, cap, e)) return;
+    if (!entries_valid(counters, sp.cap, e)) return;
+    unsigned dmin;
+    int dbits, passes;
+    view_key_shape(internal, sp.tbits, dmin, dbits, passes);
+    if (pass >= passes) return;
+    const int shift = kRadixBits * pass;
     const int64_t ntiles = ceil_div(e, kSortTile);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    {   // global exclusive digit offsets of this pass (block scan of 256 counts)
-        const unsigned c = hist_p[tid];
+    {   // global exclusive digit offsets: thread t owns digits 2t, 2t+1
+        const unsigned c0 = totals[2 * tid], c1 = totals[2 * tid + 1];
+        const unsigned c = c0 + c1;
         const unsigned inc = warp_inclusive_scan(c);
         if (lane == 31) s_scan[warp] = inc;
         __syncthreads();
         unsigned pre = 0;
         for (int w = 0; w < warp; ++w) pre += s_scan[w];
-        s_goff[tid] = pre + inc - c;
+        s_goff[2 * tid] = pre + inc - c;
+        s_goff[2 * tid + 1] = pre + inc - c + c0;
     }
     const unsigned lanemask_lt = (1u << lane) - 1u;
-    while (true) {
-        if (tid == 0) s_tile = (int64_t)atomicAdd(ticket, 1ull);
-#pragma unroll
-        for (int w = 0; w < kBlock / 32; ++w) s_wh[w][tid] = 0u;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int k = tid; k < kWarps * kBins; k += kBlock) (&s_wh[0][0])[k] = 0u;
         __syncthreads();
-        const int64_t tile = s_tile;
-        if (tile >= ntiles) break;
+        // warp w owns the contiguous items [w*512, w*512+512) of the tile, striped
         const int64_t base = tile * kSortTile + (int64_t)warp * (32 * kSortItems);
         unsigned long long key[kSortItems];
         unsigned val[kSortItems];
@@ -111,51 +198,37 @@ k_onesweep(const unsigned long long *__restrict__ kin, const unsigned *__restric
         }
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
-            const unsigned d = rank[k] == 0xffffffffu ? 256u : (unsigned)((key[k] >> shift) & 255ull);
+            const unsigned d =
+                rank[k] == 0xffffffffu ? (unsigned)kBins : digit_of(key[k], dmin, dbits, shift);
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
-            if (d < 256u && lane == leader) {
+            if (d < (unsigned)kBins && lane == leader) {
                 old = s_wh[warp][d];
                 s_wh[warp][d] = old + (unsigned)__popc(peers);
             }
             old = __shfl_sync(0xffffffffu, old, leader);
-            if (d < 256u) rank[k] = old + (unsigned)__popc(peers & lanemask_lt);
+            if (d < (unsigned)kBins) rank[k] = old + (unsigned)__popc(peers & lanemask_lt);
             __syncwarp();
         }
         __syncthreads();
-        // per digit: exclusive prefix over warps, CTA total, look-back
-        unsigned run = 0;
 #pragma unroll
-        for (int w = 0; w < kBlock / 32; ++w) {
-            const unsigned c = s_wh[w][tid];
-            s_wh[w][tid] = run;
-            run += c;
-        }
-        unsigned *my = status_p + tile * 256 + tid;
-        unsigned excl = 0;
-        if (tile == 0) {
-            st_volatile_u32(my, kInc | run);
-        } else {
-            st_volatile_u32(my, kAgg | run);
-            int64_t j = tile - 1;
-            while (true) {
-                const unsigned w = ld_volatile_u32(status_p + j * 256 + tid);
-                const unsigned fl = w & ~kCntMask;
-                if (!fl) continue;
-                excl += w & kCntMask;
-                if (fl == kInc) break;
-                --j;
+        for (int q = 0; q < kDigitsPerThread; ++q) {   // tile base + exclusive prefix over warps
+            const int d = tid + q * kBlock;
+            unsigned run = s_goff[d] + counts[tile * kBins + d];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const unsigned c = s_wh[w][d];
+                s_wh[w][d] = run;
+                run += c;
             }
-            st_volatile_u32(my, kInc | (excl + run));
         }
-        s_base[tid] = s_goff[tid] + excl;
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             if (rank[k] == 0xffffffffu) continue;
-            const unsigned d = (unsigned)((key[k] >> shift) & 255ull);
-            const unsigned pos = s_base[d] + s_wh[warp][d] + rank[k];
+            const unsigned d = digit_of(key[k], dmin, dbits, shift);
+            const unsigned pos = s_wh[warp][d] + rank[k];
             kout[pos] = key[k];
             vout[pos] = val[k];
         }
@@ -164,19 +237,22 @@ k_onesweep(const unsigned long long *__restrict__ kin, const unsigned *__restric
 }
 
 __global__ void __launch_bounds__(kBlock)
-k_ranges(const unsigned long long *__restrict__ keys, const unsigned *__restrict__ vals,
-         const int64_t *counters, int64_t cap, int64_t n_tiles, int64_t *__restrict__ starts,
-         int64_t *__restrict__ starts2, int32_t *__restrict__ entry_out) {
+k_ranges(Workspace ws, const int64_t *counters, int64_t n_tiles, int64_t *__restrict__ starts2,
+         int32_t *__restrict__ entry_out) {
     int64_t e;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-    if (!entries_valid(counters, cap, e)) {   // overflow: empty runs everywhere
+    int64_t *starts = ws.tile_starts;
+    if (!entries_valid(counters, ws.entry_capacity, e)) {   // overflow: empty runs everywhere
         for (int64_t t = gtid; t <= n_tiles; t += gsz) {
             starts[t] = 0;
             if (starts2) starts2[t] = 0;
         }
         return;
     }
+    const int fb = sorted_buffer(ws.internal);
+    const unsigned long long *keys = ws.keys[fb];
+    const unsigned *vals = ws.vals[fb];
     for (int64_t i = gtid; i <= e; i += gsz) {
         const int64_t ti = i < e ? (int64_t)(keys[i] >> 32) : n_tiles;
         const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> 32) : -1;
@@ -199,35 +275,34 @@ static int num_sms() {
     return cached;
 }
 
-int launch_sort(const ViewParams &vp, const Workspace &ws, const int64_t *counters, int *final_buf,
-                cudaStream_t st) {
+int launch_sort(const ViewParams &vp, const Workspace &ws, const int64_t *counters, cudaStream_t st) {
     const int64_t n_tiles = (int64_t)vp.tiles_x * vp.tiles_y;
-    const int passes = sort_passes((int)n_tiles);
-    const int64_t cap = ws.entry_capacity;
+    SortParams sp{ws.entry_capacity, tile_bits(n_tiles)};
+    const int max_passes = sort_passes((int)n_tiles);
     const int sms = num_sms();
-    const unsigned hist_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kBlock), sms * 4));
-    k_sort_hist<<<hist_grid, kBlock, 0, st>>>(ws.keys[0], counters, cap, passes, ws.hist,
-                                              ws.sort_status, ws.sort_tiles_cap);
+    // one CTA per 4096-key tile of the capacity (idle ones exit), grid-stride beyond
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ws.sort_tiles_cap, sms * 8));
     int src = 0;
-    const unsigned sweep_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ws.sort_tiles_cap, sms * 3));
-    for (int p = 0; p < passes; ++p) {
-        k_onesweep<<<sweep_grid, kBlock, 0, st>>>(
-            ws.keys[src], ws.vals[src], ws.keys[1 - src], ws.vals[1 - src], counters, cap, 8 * p,
-            ws.hist + p * 256, ws.sort_status + (int64_t)p * ws.sort_tiles_cap * 256,
-            reinterpret_cast<unsigned long long *>(&ws.internal[kTicketSortBase + p]));
+    for (int p = 0; p < max_passes; ++p) {
+        unsigned *counts = ws.sort_status + (int64_t)p * ws.sort_tiles_cap * kBins;
+        unsigned *totals = ws.hist + p * kBins;
+        k_upsweep<<<grid, kBlock, 0, st>>>(ws.keys[src], counters, sp, ws.internal, p, counts, totals);
+        k_colscan<<<kBins / 32, kBlock, 0, st>>>(counters, sp, ws.internal, p, counts);
+        k_downsweep<<<grid, kBlock, 0, st>>>(ws.keys[src], ws.vals[src], ws.keys[1 - src],
+                                             ws.vals[1 - src], counters, sp, ws.internal, p, counts,
+                                             totals);
         src = 1 - src;
     }
-    *final_buf = src;
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
-int launch_ranges(const ViewParams &vp, const Workspace &ws, const int64_t *counters, int buf,
+int launch_ranges(const ViewParams &vp, const Workspace &ws, const int64_t *counters,
                   int64_t *tile_starts_out, int32_t *entry_splat_out, cudaStream_t st) {
     const int64_t n_tiles = (int64_t)vp.tiles_x * vp.tiles_y;
     const int64_t cap = ws.entry_capacity;
-    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap + 1, kBlock), num_sms() * 4));
-    k_ranges<<<rgrid, kBlock, 0, st>>>(ws.keys[buf], ws.vals[buf], counters, cap, n_tiles,
-                                       ws.tile_starts, tile_starts_out, entry_splat_out);
+    const unsigned rgrid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap + 1, kBlock), num_sms() * 4));
+    k_ranges<<<rgrid, kBlock, 0, st>>>(ws, counters, n_tiles, tile_starts_out, entry_splat_out);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
