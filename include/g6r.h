@@ -172,16 +172,18 @@ void g6r_profiler_reset(g6r_profiler *prof);
  * summed per-stage milliseconds, *views the number of views recorded. */
 int g6r_profiler_read(g6r_profiler *prof, double *stage_ms, int32_t *views);
 
-/* Render `count` views of one scene (same image size) into frames[k].  Up to
- * `concurrency` views (1..8) are in flight at once on internal side streams
- * forked from and joined back into `stream`; the workspace must hold
- * concurrency x g6r_workspace_bytes(...).  final_t / last_contrib may be
- * NULL in these frames.  prof may be NULL. */
+/* Render `count` views of one scene (same image size) into frames[k], in
+ * batches of `batch` views (1..8): every stage kernel processes a whole batch
+ * per launch (grid = work x views), so one view's long tile runs overlap the
+ * other views' work and the projection shares the record stream through L2.
+ * The workspace must hold batch x g6r_workspace_bytes(...).  final_t /
+ * last_contrib may be NULL in these frames.  prof may be NULL; it records one
+ * slot per batch. */
 int g6r_render_views(const g6r_scene *scene, uint32_t group_mask,
                      const g6r_camera *cams /* host array */, int32_t count,
                      const g6r_config *cfg, void *workspace, size_t workspace_bytes,
                      int64_t entry_capacity, const g6r_frame *frames /* host array */,
-                     int32_t concurrency, g6r_profiler *prof, g6r_stream_t stream);
+                     int32_t batch, g6r_profiler *prof, g6r_stream_t stream);
 
 /* Test probe: y[i] = the device expf used by the f32 compositor (glibc
  * algorithm, g6r_common.cuh) for n floats. */

@@ -1,15 +1,16 @@
 // g6r_api.cu -- extern "C" boundary of libg6r.so (declared in include/g6r.h).
 //
 // Validates arguments, carves the caller's workspace, and enqueues the stage
-// kernels on the caller's stream.  Never allocates, never synchronises.
+// kernels on the caller's stream.  Never allocates device memory, never
+// synchronises (except g6r_profiler_read, which waits on its own events).
+// Views are rendered in batches: every stage kernel takes up to kMaxBatch views
+// per launch (grid = work x views).
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
-#include <map>
-#include <mutex>
 #include <string>
-#include <vector>
 
 #include "g6r_common.cuh"
 #include "g6r_internal.h"
@@ -39,10 +40,11 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_status, total;
+        sort_counts, total;
     int64_t sort_tiles_cap;
 };
 
+// Per-view workspace layout.  [0, clear_end) is zeroed before every view.
 static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     Layout L{};
     size_t o = 0;
@@ -52,7 +54,7 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + kMaxPasses * kBins * sizeof(unsigned));
     L.proj = o;
     const int64_t nblk = ceil_div(n > 0 ? n : 1, kBlock);
-    o = align_up(o + 4 * nblk * sizeof(unsigned long long));
+    o = align_up(o + nblk * sizeof(unsigned long long));
     L.clear_end = o;
     L.tile_starts = o;
     o = align_up(o + (tiles + 1) * sizeof(int64_t));
@@ -67,30 +69,25 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     L.vals1 = o;
     o = align_up(o + (size_t)cap * 4);
     L.sort_tiles_cap = ceil_div(cap > 0 ? cap : 1, kSortTile);
-    L.sort_status = o;
+    L.sort_counts = o;
     o = align_up(o + (size_t)kMaxPasses * L.sort_tiles_cap * kBins * sizeof(unsigned));
     L.total = o;
     return L;
 }
 
-static Workspace carve(void *base, const Layout &L, int64_t n, int64_t cap) {
+static Workspace carve(void *base, const Layout &L, int64_t cap) {
     char *b = static_cast<char *>(base);
     Workspace w{};
     w.internal = reinterpret_cast<long long *>(b + L.internal);
     w.hist = reinterpret_cast<unsigned *>(b + L.hist);
-    const int64_t nblk = ceil_div(n > 0 ? n : 1, kBlock);
-    unsigned long long *p = reinterpret_cast<unsigned long long *>(b + L.proj);
-    w.proj_agg_m = p;
-    w.proj_agg_e = p + nblk;
-    w.proj_inc_m = p + 2 * nblk;
-    w.proj_inc_e = p + 3 * nblk;
+    w.proj_status = reinterpret_cast<unsigned long long *>(b + L.proj);
     w.tile_starts = reinterpret_cast<int64_t *>(b + L.tile_starts);
     w.payload = b + L.payload;
     w.keys[0] = reinterpret_cast<unsigned long long *>(b + L.keys0);
     w.keys[1] = reinterpret_cast<unsigned long long *>(b + L.keys1);
     w.vals[0] = reinterpret_cast<unsigned *>(b + L.vals0);
     w.vals[1] = reinterpret_cast<unsigned *>(b + L.vals1);
-    w.sort_status = reinterpret_cast<unsigned *>(b + L.sort_status);
+    w.sort_counts = reinterpret_cast<unsigned *>(b + L.sort_counts);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;
     return w;
@@ -134,10 +131,10 @@ static int make_view(const g6r_camera *cam, const g6r_config *cfg, ViewParams &v
     return G6R_OK;
 }
 
-static int check_ws(const Layout &L, void *ws, size_t bytes) {
-    if (!ws && L.total) return fail(G6R_EINVAL, "workspace is NULL");
-    if (bytes < L.total)
-        return fail(G6R_EINVAL, "workspace too small: %zu bytes given, %zu needed", bytes, L.total);
+static int check_ws(size_t need, void *ws, size_t bytes) {
+    if (!ws && need) return fail(G6R_EINVAL, "workspace is NULL");
+    if (bytes < need)
+        return fail(G6R_EINVAL, "workspace too small: %zu bytes given, %zu needed", bytes, need);
     if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(G6R_EINVAL, "workspace must be 256-byte aligned");
     return G6R_OK;
 }
@@ -148,72 +145,80 @@ static int check_cap(int64_t cap) {
     return G6R_OK;
 }
 
+// zero the batch's per-view scratch heads and counters in one launch
+__global__ void k_clear(const __grid_constant__ Batch b, size_t clear_words) {
+    const int v = blockIdx.y;
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(b.ws[v].internal);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < clear_words;
+         i += (size_t)gridDim.x * blockDim.x)
+        w[i] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x < G6R_NCOUNTERS) b.out[v].counters[threadIdx.x] = 0;
+}
+
+int launch_clear(const Batch &b, size_t clear_bytes, cudaStream_t st) {
+    const size_t words = clear_bytes / 8;
+    const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>((words + 255) / 256, 64));
+    k_clear<<<dim3(gx, b.nviews), 256, 0, st>>>(b, words);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
 }  // namespace g6r
 
 struct g6r_profiler {
-    int32_t max_views = 0, used = 0;
-    cudaEvent_t *ev = nullptr;   // (max_views) x (G6R_NSTAGES + 1)
+    int32_t max_batches = 0, used = 0, views = 0;
+    cudaEvent_t *ev = nullptr;   // (max_batches) x (G6R_NSTAGES + 1)
+    int32_t *nv = nullptr;       // views per recorded batch
 };
 
 namespace g6r {
 
 static void prof_mark(g6r_profiler *p, int k, cudaStream_t st) {
-    if (p && p->used < p->max_views) cudaEventRecord(p->ev[p->used * (G6R_NSTAGES + 1) + k], st);
+    if (p && p->used < p->max_batches) cudaEventRecord(p->ev[p->used * (G6R_NSTAGES + 1) + k], st);
 }
 
-constexpr int kMaxSlots = 8;
-
-// Side streams for concurrent views, created once per device and reused.
-static int side_streams(int n, cudaStream_t *out) {
-    static std::mutex mu;
-    static std::map<int, std::vector<cudaStream_t>> pool;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
-    std::lock_guard<std::mutex> lock(mu);
-    std::vector<cudaStream_t> &v = pool[dev];
-    while ((int)v.size() < n) {
-        cudaStream_t s;
-        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
-            return cuda_check("cudaStreamCreate");
-        v.push_back(s);
-    }
-    for (int i = 0; i < n; ++i) out[i] = v[i];
-    return G6R_OK;
-}
-
-static int render_one(const g6r_scene *scene, uint32_t mask, const g6r_camera *cam,
-                      const g6r_config *cfg, void *ws_base, size_t ws_bytes, int64_t cap,
-                      const g6r_frame *fr, const g6r_splat_out *splats, cudaStream_t st,
-                      g6r_profiler *prof = nullptr) {
+// Render one batch of views (all stages, CUDA events between them when profiled).
+static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera *cams, int nviews,
+                        const g6r_config *cfg, void *ws_base, size_t ws_bytes, int64_t cap,
+                        const g6r_frame *frames, const g6r_splat_out *splats, cudaStream_t st,
+                        g6r_profiler *prof) {
     if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL or has negative size");
     if (scene->n > 0 && (!scene->records || !scene->flags)) return fail(G6R_EINVAL, "scene arrays are NULL");
-    if (!fr || !fr->image || !fr->counters)
-        return fail(G6R_EINVAL, "frame outputs image/counters are required");
+    if (nviews < 1 || nviews > kMaxBatch) return fail(G6R_EINVAL, "batch of %d views", nviews);
     if (int rc = check_cap(cap)) return rc;
-    ViewParams vp;
-    if (int rc = make_view(cam, cfg, vp)) return rc;
-    const int64_t tiles = (int64_t)vp.tiles_x * vp.tiles_y;
-    const Layout L = layout(scene->n, tiles, cap, vp.precision);
-    if (int rc = check_ws(L, ws_base, ws_bytes)) return rc;
-    Workspace ws = carve(ws_base, L, scene->n, cap);
-    if (cudaMemsetAsync(ws_base, 0, L.clear_end, st) != cudaSuccess ||
-        cudaMemsetAsync(fr->counters, 0, G6R_NCOUNTERS * sizeof(int64_t), st) != cudaSuccess)
-        return cuda_check("memset");
+    Batch b;
+    memset(&b, 0, sizeof b);
+    b.nviews = nviews;
+    for (int v = 0; v < nviews; ++v) {
+        const g6r_frame *fr = &frames[v];
+        if (!fr->image || !fr->counters)
+            return fail(G6R_EINVAL, "frame outputs image/counters are required");
+        if (int rc = make_view(&cams[v], cfg, b.vp[v])) return rc;
+        if (b.vp[v].iw != b.vp[0].iw || b.vp[v].ih != b.vp[0].ih)
+            return fail(G6R_EINVAL, "views of one batch must share the image size");
+    }
+    const int64_t tiles = (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y;
+    const Layout L = layout(scene->n, tiles, cap, cfg->precision);
+    if (int rc = check_ws(L.total * nviews, ws_base, ws_bytes)) return rc;
+    for (int v = 0; v < nviews; ++v) {
+        b.ws[v] = carve(static_cast<char *>(ws_base) + L.total * v, L, cap);
+        b.out[v] = ViewOut{frames[v].image, frames[v].final_t, frames[v].last_contrib,
+                           frames[v].counters, frames[v].entry_splat, frames[v].tile_starts};
+    }
+    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     prof_mark(prof, 0, st);
-    int rc = launch_project(*scene, mask, vp, ws, fr->counters, splats, true, st);
-    if (rc) return cuda_check("project");
+    if (launch_project(*scene, mask, b, nviews == 1 ? splats : nullptr, true, st))
+        return cuda_check("project");
     prof_mark(prof, 1, st);
-    rc = launch_sort(vp, ws, fr->counters, st);
-    if (rc) return cuda_check("sort");
+    if (launch_sort(b, st)) return cuda_check("sort");
     prof_mark(prof, 2, st);
-    rc = launch_ranges(vp, ws, fr->counters, fr->tile_starts, fr->entry_splat, st);
-    if (rc) return cuda_check("ranges");
+    if (launch_ranges(b, st)) return cuda_check("ranges");
     prof_mark(prof, 3, st);
-    rc = launch_composite(vp, ws.payload, ws.vals[0], ws.vals[1], ws.internal, ws.tile_starts, fr->image, fr->final_t,
-                          fr->last_contrib, st);
-    if (rc) return cuda_check("composite");
+    if (launch_composite(b, true, st)) return cuda_check("composite");
     prof_mark(prof, 4, st);
-    if (prof && prof->used < prof->max_views) ++prof->used;
+    if (prof && prof->used < prof->max_batches) {
+        prof->nv[prof->used++] = nviews;
+        prof->views += nviews;
+    }
     return G6R_OK;
 }
 
@@ -223,7 +228,7 @@ using namespace g6r;
 
 extern "C" {
 
-const char *g6r_version(void) { return "g6r 0.1.0 sm_100a"; }
+const char *g6r_version(void) { return "g6r 0.2.0 sm_100a"; }
 
 const char *g6r_last_error(void) { return t_err.c_str(); }
 
@@ -242,6 +247,7 @@ int g6r_prepare(int64_t n, const double *mu_p, const double *mu_d, const double 
     if (!spatial_scale || !label_counts) return fail(G6R_EINVAL, "spatial_scale/label_counts are required");
     if (n > 0 && (!mu_p || !mu_d || !cov_raw || !sh || !opacity_raw || !labels || !records || !flags))
         return fail(G6R_EINVAL, "NULL scene array");
+    if (n >= (1ll << 30)) return fail(G6R_EINVAL, "scenes are limited to 2^30 Gaussians");
     if (launch_prepare(n, mu_p, mu_d, cov_raw, sh, opacity_raw, labels, spatial_scale,
                        directional_scale, w_mode, records, flags, label_counts, (cudaStream_t)stream))
         return cuda_check("prepare");
@@ -264,72 +270,41 @@ int g6r_render(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *ca
                const g6r_config *cfg, void *workspace, size_t workspace_bytes,
                int64_t entry_capacity, const g6r_frame *frame, const g6r_splat_out *splats,
                g6r_stream_t stream) {
-    return render_one(scene, group_mask, cam, cfg, workspace, workspace_bytes, entry_capacity,
-                      frame, splats, (cudaStream_t)stream);
+    if (!frame) return fail(G6R_EINVAL, "frame is NULL");
+    if (int rc = check_config(cfg)) return rc;
+    return render_batch(scene, group_mask, cam, 1, cfg, workspace, workspace_bytes, entry_capacity,
+                        frame, splats, (cudaStream_t)stream, nullptr);
 }
 
 int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cams,
                      int32_t count, const g6r_config *cfg, void *workspace,
                      size_t workspace_bytes, int64_t entry_capacity, const g6r_frame *frames,
-                     int32_t concurrency, g6r_profiler *prof, g6r_stream_t stream) {
+                     int32_t batch, g6r_profiler *prof, g6r_stream_t stream) {
     if (count < 0 || (count > 0 && (!cams || !frames))) return fail(G6R_EINVAL, "bad view list");
     if (count == 0) return G6R_OK;
-    if (!scene || !cfg) return fail(G6R_EINVAL, "scene/config is NULL");
     if (int rc = check_config(cfg)) return rc;
-    int slots = concurrency < 1 ? 1 : (concurrency > kMaxSlots ? kMaxSlots : concurrency);
-    if (slots > count) slots = count;
-    const int64_t tiles = (int64_t)((cams[0].width + cfg->tile_size - 1) / cfg->tile_size) *
-                          ((cams[0].height + cfg->tile_size - 1) / cfg->tile_size);
-    const size_t per = layout(scene->n, tiles, entry_capacity, cfg->precision).total;
-    if (workspace_bytes < per * slots)
-        return fail(G6R_EINVAL, "workspace too small for %d concurrent views: %zu < %zu", slots,
-                    workspace_bytes, per * slots);
-    cudaStream_t main = (cudaStream_t)stream;
-    if (slots == 1) {
-        for (int32_t k = 0; k < count; ++k) {
-            const int rc = render_one(scene, group_mask, &cams[k], cfg, workspace, per,
-                                      entry_capacity, &frames[k], nullptr, main, prof);
-            if (rc) return rc;
-        }
-        return G6R_OK;
+    const int nb = batch < 1 ? 1 : (batch > kMaxBatch ? kMaxBatch : batch);
+    for (int32_t k = 0; k < count; k += nb) {
+        const int nv = count - k < nb ? count - k : nb;
+        const int rc = render_batch(scene, group_mask, &cams[k], nv, cfg, workspace, workspace_bytes,
+                                    entry_capacity, &frames[k], nullptr, (cudaStream_t)stream, prof);
+        if (rc) return rc;
     }
-    // Views are independent: spread them over `slots` side streams, each with
-    // its own workspace slice, so one view's long tile runs overlap the next
-    // view's projection and sort instead of idling the other SMs.
-    cudaStream_t side[kMaxSlots];
-    if (int rc = side_streams(slots, side)) return rc;
-    cudaEvent_t fork;
-    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return cuda_check("event");
-    cudaEventRecord(fork, main);
-    for (int s = 0; s < slots; ++s) cudaStreamWaitEvent(side[s], fork, 0);
-    cudaEventDestroy(fork);
-    int rc = G6R_OK;
-    for (int32_t k = 0; k < count && rc == G6R_OK; ++k) {
-        const int s = k % slots;
-        rc = render_one(scene, group_mask, &cams[k], cfg, static_cast<char *>(workspace) + per * s,
-                        per, entry_capacity, &frames[k], nullptr, side[s], prof);
-    }
-    for (int s = 0; s < slots; ++s) {   // join (also on error, so the streams stay ordered)
-        cudaEvent_t j;
-        if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
-            cudaEventRecord(j, side[s]);
-            cudaStreamWaitEvent(main, j, 0);
-            cudaEventDestroy(j);
-        }
-    }
-    return rc;
+    return G6R_OK;
 }
 
-g6r_profiler *g6r_profiler_create(int32_t max_views) {
-    if (max_views <= 0) return nullptr;
+g6r_profiler *g6r_profiler_create(int32_t max_batches) {
+    if (max_batches <= 0) return nullptr;
     g6r_profiler *p = new g6r_profiler;
-    p->max_views = max_views;
-    const int ne = max_views * (G6R_NSTAGES + 1);
+    p->max_batches = max_batches;
+    const int ne = max_batches * (G6R_NSTAGES + 1);
     p->ev = new cudaEvent_t[ne];
+    p->nv = new int32_t[max_batches];
     for (int k = 0; k < ne; ++k) {
         if (cudaEventCreate(&p->ev[k]) != cudaSuccess) {
             for (int j = 0; j < k; ++j) cudaEventDestroy(p->ev[j]);
             delete[] p->ev;
+            delete[] p->nv;
             delete p;
             fail(G6R_ECUDA, "cudaEventCreate failed");
             return nullptr;
@@ -340,19 +315,20 @@ g6r_profiler *g6r_profiler_create(int32_t max_views) {
 
 void g6r_profiler_destroy(g6r_profiler *p) {
     if (!p) return;
-    for (int k = 0; k < p->max_views * (G6R_NSTAGES + 1); ++k) cudaEventDestroy(p->ev[k]);
+    for (int k = 0; k < p->max_batches * (G6R_NSTAGES + 1); ++k) cudaEventDestroy(p->ev[k]);
     delete[] p->ev;
+    delete[] p->nv;
     delete p;
 }
 
 void g6r_profiler_reset(g6r_profiler *p) {
-    if (p) p->used = 0;
+    if (p) p->used = p->views = 0;
 }
 
 int g6r_profiler_read(g6r_profiler *p, double *stage_ms, int32_t *views) {
     if (!p || !stage_ms || !views) return fail(G6R_EINVAL, "NULL profiler argument");
     for (int s = 0; s < G6R_NSTAGES; ++s) stage_ms[s] = 0.0;
-    *views = p->used;
+    *views = p->views;
     if (!p->used) return G6R_OK;
     if (cudaEventSynchronize(p->ev[p->used * (G6R_NSTAGES + 1) - 1]) != cudaSuccess)
         return cuda_check("profiler sync");
@@ -376,16 +352,17 @@ int g6r_project(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *c
                 int64_t *counters, const g6r_splat_out *splats, g6r_stream_t stream) {
     if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL");
     if (!counters) return fail(G6R_EINVAL, "counters are required");
-    ViewParams vp;
-    if (int rc = make_view(cam, cfg, vp)) return rc;
-    const Layout L = layout(scene->n, (int64_t)vp.tiles_x * vp.tiles_y, 0, vp.precision);
-    if (int rc = check_ws(L, workspace, workspace_bytes)) return rc;
-    Workspace ws = carve(workspace, L, scene->n, 0);
+    Batch b;
+    memset(&b, 0, sizeof b);
+    b.nviews = 1;
+    if (int rc = make_view(cam, cfg, b.vp[0])) return rc;
+    const Layout L = layout(scene->n, (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y, 0, b.vp[0].precision);
+    if (int rc = check_ws(L.total, workspace, workspace_bytes)) return rc;
+    b.ws[0] = carve(workspace, L, 0);
+    b.out[0].counters = counters;
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(workspace, 0, L.clear_end, st) != cudaSuccess ||
-        cudaMemsetAsync(counters, 0, G6R_NCOUNTERS * sizeof(int64_t), st) != cudaSuccess)
-        return cuda_check("memset");
-    if (launch_project(*scene, group_mask, vp, ws, counters, splats, false, st)) return cuda_check("project");
+    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
+    if (launch_project(*scene, group_mask, b, splats, false, st)) return cuda_check("project");
     return G6R_OK;
 }
 
@@ -399,23 +376,26 @@ int g6r_bin(int64_t m, const double *means2d, const int32_t *radii, const double
     if (int rc = check_cap(entry_capacity)) return rc;
     if (width < 1 || height < 1) return fail(G6R_EINVAL, "width and height must be positive");
     if (tile_size < 1) return fail(G6R_EINVAL, "tile_size must be positive");
-    ViewParams vp{};
+    Batch b;
+    memset(&b, 0, sizeof b);
+    b.nviews = 1;
+    ViewParams &vp = b.vp[0];
     vp.iw = width;
     vp.ih = height;
     vp.tile_size = tile_size;
     vp.tiles_x = (width + tile_size - 1) / tile_size;
     vp.tiles_y = (height + tile_size - 1) / tile_size;
     const Layout L = layout(m, (int64_t)vp.tiles_x * vp.tiles_y, entry_capacity, 0);
-    if (int rc = check_ws(L, workspace, workspace_bytes)) return rc;
-    Workspace ws = carve(workspace, L, m, entry_capacity);
+    if (int rc = check_ws(L.total, workspace, workspace_bytes)) return rc;
+    b.ws[0] = carve(workspace, L, entry_capacity);
+    b.out[0].counters = counters;
+    b.out[0].entry_splat = entry_splat;
+    b.out[0].tile_starts = tile_starts;
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(workspace, 0, L.clear_end, st) != cudaSuccess ||
-        cudaMemsetAsync(counters, 0, G6R_NCOUNTERS * sizeof(int64_t), st) != cudaSuccess)
-        return cuda_check("memset");
-    if (launch_duplicate(m, means2d, radii, depths, vp, ws, counters, st)) return cuda_check("duplicate");
-    int final_buf = 0;
-    if (launch_sort(vp, ws, counters, st)) return cuda_check("sort");
-    if (launch_ranges(vp, ws, counters, tile_starts, entry_splat, st)) return cuda_check("ranges");
+    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
+    if (launch_duplicate(m, means2d, radii, depths, b, st)) return cuda_check("duplicate");
+    if (launch_sort(b, st)) return cuda_check("sort");
+    if (launch_ranges(b, st)) return cuda_check("ranges");
     return G6R_OK;
 }
 
@@ -431,21 +411,27 @@ int g6r_composite(int64_t m, int32_t precision, const void *means2d, const void 
         return fail(G6R_EINVAL, "tiles_x/tiles_y do not match width/height/tile_size");
     if (!image || !final_t || !last_contrib || !tile_starts) return fail(G6R_EINVAL, "NULL output");
     const Layout L = layout(m, (int64_t)tiles_x * tiles_y, 0, precision);
-    if (int rc = check_ws(L, workspace, workspace_bytes)) return rc;
-    Workspace ws = carve(workspace, L, m, 0);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (launch_pack_payload(m, precision, means2d, conics, colors, alphas, ws.payload, st))
-        return cuda_check("pack_payload");
-    ViewParams vp{};
+    if (int rc = check_ws(L.total, workspace, workspace_bytes)) return rc;
+    Batch b;
+    memset(&b, 0, sizeof b);
+    b.nviews = 1;
+    ViewParams &vp = b.vp[0];
     vp.iw = width;
     vp.ih = height;
     vp.tile_size = tile_size;
     vp.tiles_x = tiles_x;
     vp.tiles_y = tiles_y;
     vp.precision = precision;
-    if (launch_composite(vp, ws.payload, reinterpret_cast<const unsigned *>(entry_splat), nullptr, nullptr, tile_starts,
-                         image, final_t, last_contrib, st))
-        return cuda_check("composite");
+    b.ws[0] = carve(workspace, L, 0);
+    b.ws[0].vals[0] = const_cast<unsigned *>(reinterpret_cast<const unsigned *>(entry_splat));
+    b.ws[0].tile_starts = const_cast<int64_t *>(tile_starts);
+    b.out[0].image = image;
+    b.out[0].final_t = final_t;
+    b.out[0].last_contrib = last_contrib;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (launch_pack_payload(m, precision, means2d, conics, colors, alphas, b.ws[0].payload, st))
+        return cuda_check("pack_payload");
+    if (launch_composite(b, false, st)) return cuda_check("composite");
     return G6R_OK;
 }
 

@@ -83,6 +83,28 @@ __device__ __forceinline__ void cull_extents(double a, double b, double c, doubl
     ey = (float)(3.0 * sqrt(a / det) * grow + 1e-3);
 }
 
+// Same extents for an f32 conic, in float arithmetic (the determinant exactly
+// from the f32 products in double).  The float evaluation adds at most a few
+// ulp (~1e-6 relative); the extra 1e-5 relative growth absorbs it.
+__device__ __forceinline__ void cull_extents_f32(float a, float b, float c, float &ex, float &ey) {
+    const double detd = (double)a * (double)c - (double)b * (double)b;
+    const float inf = __int_as_float(0x7f800000);
+    if (!(detd > 0.0) || !(a > 0.0f) || !(c > 0.0f)) {
+        ex = ey = inf;
+        return;
+    }
+    const float inv = 1.0f / (float)detd;
+    const float kappa = (a + c) * (a + c) * 0.25f * inv;
+    const float delta = 64.0f * 0x1p-23f * kappa + 1e-5f;
+    if (!(delta < 0.5f)) {
+        ex = ey = inf;
+        return;
+    }
+    const float grow = 1.0f + delta;
+    ex = 3.0f * sqrtf(c * inv) * grow + 1e-3f;
+    ey = 3.0f * sqrtf(a * inv) * grow + 1e-3f;
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // --- glibc-compatible expf --------------------------------------------------

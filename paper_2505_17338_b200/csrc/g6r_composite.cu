@@ -23,30 +23,65 @@ __constant__ unsigned long long c_expf_tab[32] = G6R_EXPF_TABLE;
 template <typename Real>
 struct Px;
 
+// Shared-memory splat record: two 16-byte vectors + the blue channel, so the
+// per-hit reads are LDS.128 x2 (+1) instead of nine scalar loads.
 template <>
 struct Px<float> {
     using Payload = PayloadF32;
-    struct S {   // unpacked splat in shared memory
-        float mx, my, ca, cb, cc, alpha, r, g, b;
+    struct alignas(16) S {
+        float4 a;   // mx, my, conic a, conic b
+        float4 b;   // conic c, alpha, r, g
+        float c;    // b
     };
     __device__ static S unpack(const Payload &p, float &ex, float &ey) {
         ex = p.c.y;
         ey = p.c.z;
-        return S{p.a.x, p.a.y, p.a.z, p.a.w, p.b.x, p.b.y, p.b.z, p.b.w, p.c.x};
+        S s;
+        s.a = p.a;
+        s.b = p.b;
+        s.c = p.c.x;
+        return s;
     }
+    __device__ static float mx(const S &s) { return s.a.x; }
+    __device__ static float my(const S &s) { return s.a.y; }
 };
 template <>
 struct Px<double> {
     using Payload = PayloadF64;
-    struct S {
-        double mx, my, ca, cb, cc, alpha, r, g, b;
+    struct alignas(16) S {
+        double2 a, b, c, d;   // (mx,my) (ca,cb) (cc,alpha) (r,g)
+        double e;             // b
     };
     __device__ static S unpack(const Payload &p, float &ex, float &ey) {
         ex = (float)p.e.y;
         ey = (float)p.f.x;
-        return S{p.a.x, p.a.y, p.b.x, p.b.y, p.c.x, p.c.y, p.d.x, p.d.y, p.e.x};
+        S s;
+        s.a = p.a;
+        s.b = p.b;
+        s.c = p.c;
+        s.d = p.d;
+        s.e = p.e.x;
+        return s;
     }
+    __device__ static double mx(const S &s) { return s.a.x; }
+    __device__ static double my(const S &s) { return s.a.y; }
 };
+
+// Field access common to both layouts.
+__device__ __forceinline__ void fields(const Px<float>::S &s, float &mx, float &my, float &ca,
+                                       float &cb, float &cc, float &al) {
+    mx = s.a.x; my = s.a.y; ca = s.a.z; cb = s.a.w; cc = s.b.x; al = s.b.y;
+}
+__device__ __forceinline__ void colours(const Px<float>::S &s, float &r, float &g, float &b) {
+    r = s.b.z; g = s.b.w; b = s.c;
+}
+__device__ __forceinline__ void fields(const Px<double>::S &s, double &mx, double &my, double &ca,
+                                       double &cb, double &cc, double &al) {
+    mx = s.a.x; my = s.a.y; ca = s.b.x; cb = s.b.y; cc = s.c.x; al = s.c.y;
+}
+__device__ __forceinline__ void colours(const Px<double>::S &s, double &r, double &g, double &b) {
+    r = s.d.x; g = s.d.y; b = s.e;
+}
 
 // Pixel of thread t in a tile: 16x16 tiles give each warp an 8x4 block (so the
 // per-warp culling box is square-ish); other tile sizes are row-major.
@@ -66,19 +101,39 @@ __device__ __forceinline__ float splat_exp(float x, const unsigned long long *ta
 }
 __device__ __forceinline__ double splat_exp(double x, const unsigned long long *) { return exp(x); }
 
-template <typename Real>
-__global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__restrict__ payload,
-                            const unsigned *vals0, const unsigned *vals1, const long long *sel,
-                            const int64_t *__restrict__ starts,
-                            Real *__restrict__ image, Real *__restrict__ final_t,
-                            int32_t *__restrict__ last_contrib) {
+// One CTA per tile, one thread per pixel.  kNB > 0: compile-time block size
+// (16x16 tiles, static shared memory); kNB == 0: any tile size up to 32x32.
+//
+// The run is consumed in batches of blockDim entries, double-buffered: the
+// gather of batch k+1 (payload[vals[e]], L2-resident) is issued into registers
+// before batch k is composited and lands in the other shared buffer after, so
+// its latency hides behind compute and each batch costs one barrier.  The
+// staging thread also tests the splat's conservative 3-sigma box against every
+// warp's pixel block; warps then ballot over the batch and visit only splats
+// that can touch them, in ascending order (the per-pixel order, hence every
+// bit, is unchanged).
+template <typename Real, int kNB>
+__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024)
+k_composite(const __grid_constant__ Batch bt, int sorted) {
     using S = typename Px<Real>::S;
+    const int view = blockIdx.y;
+    const ViewParams &vp = bt.vp[view];
+    const Workspace &wsv = bt.ws[view];
+    const typename Px<Real>::Payload *__restrict__ payload =
+        static_cast<const typename Px<Real>::Payload *>(wsv.payload);
+    const int64_t *__restrict__ starts = wsv.tile_starts;
+    Real *__restrict__ image = static_cast<Real *>(bt.out[view].image);
+    Real *__restrict__ final_t = static_cast<Real *>(bt.out[view].final_t);
+    int32_t *__restrict__ last_contrib = bt.out[view].last_contrib;
+    constexpr int kStatic = kNB > 0 ? kNB : 1;
+    __shared__ S s_sp_static[kNB > 0 ? 2 * kStatic : 1];
+    __shared__ unsigned s_mask_static[kNB > 0 ? 2 * kStatic : 1];
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int nb = blockDim.x;
-    S *sp = reinterpret_cast<S *>(smem_raw);
-    unsigned *smask = reinterpret_cast<unsigned *>(sp + nb);   // warps each splat can touch
+    const int nb = kNB > 0 ? kNB : (int)blockDim.x;
+    S *sp = kNB > 0 ? s_sp_static : reinterpret_cast<S *>(smem_raw);
+    unsigned *smask = kNB > 0 ? s_mask_static : reinterpret_cast<unsigned *>(sp + 2 * nb);
     __shared__ unsigned long long s_tab[32];
-    __shared__ float4 s_wbox[32];                             // pixel-centre box per warp
+    __shared__ float4 s_wbox[32];   // pixel-centre box per warp
     if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
 
     const int ts = vp.tile_size;
@@ -114,7 +169,7 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
         s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
                                            : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
     }
-    const unsigned *__restrict__ vals = (sel && sorted_buffer(sel)) ? vals1 : vals0;
+    const unsigned *__restrict__ vals = wsv.vals[sorted ? sorted_buffer(wsv.internal) : 0];
     const int64_t lo = starts[tile], hi = starts[tile + 1];
     const Real fx = (Real)px, fy = (Real)py;
     const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
@@ -122,49 +177,65 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
     Real T = one, ar = 0, ag = 0, ab = 0, aa = 0;
     int last = 0;
     bool done = !inside;
-    for (int64_t b0 = lo; b0 < hi; b0 += nb) {
-        __syncthreads();   // previous batch consumed; s_tab / s_wbox ready
-        const int64_t e = b0 + threadIdx.x;
-        if (e < hi) {
-            float ex, ey;
-            const S s = Px<Real>::unpack(payload[vals[e]], ex, ey);
-            sp[threadIdx.x] = s;
-            const float mx = (float)s.mx, my = (float)s.my;
-            unsigned m = 0;
-            for (int w = 0; w < nwarps; ++w) {
-                const float4 bx = s_wbox[w];
-                if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w)
-                    m |= 1u << w;
-            }
-            smask[threadIdx.x] = m;
+    __syncthreads();   // s_wbox / s_tab ready
+
+    // stage batch k's entry (this thread's) into buffer `buf`
+    auto stage = [&](int64_t b0, int buf, const typename Px<Real>::Payload &pl, bool have) {
+        if (!have) return;
+        float ex, ey;
+        const S s = Px<Real>::unpack(pl, ex, ey);
+        sp[buf * nb + threadIdx.x] = s;
+        const float mx = (float)Px<Real>::mx(s), my = (float)Px<Real>::my(s);
+        unsigned m = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            const float4 bx = s_wbox[w];
+            if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) m |= 1u << w;
         }
-        __syncthreads();
+        smask[buf * nb + threadIdx.x] = m;
+    };
+
+    typename Px<Real>::Payload pre;
+    bool have = lo + threadIdx.x < hi;
+    if (have) pre = payload[vals[lo + threadIdx.x]];
+    stage(lo, 0, pre, have);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t b0 = lo; b0 < hi; b0 += nb, buf ^= 1) {
+        // issue the next batch's gather now; it lands while this batch composites
+        const int64_t e1 = b0 + nb + threadIdx.x;
+        const bool have1 = e1 < hi;
+        if (have1) pre = payload[vals[e1]];
+        const S *bsp = sp + buf * nb;
+        const unsigned *bmask = smask + buf * nb;
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
         if (!__all_sync(wmask, done)) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
-                // ballot over the splats c0..c0+31 (one per lane, any warp width)
-                unsigned hits = 0;
+                unsigned hits = 0;   // splats c0..c0+31 that can touch this warp
                 for (int k = 0; k < 32; k += wlanes) {
                     const int jl = c0 + k + lane;
                     const unsigned b = __ballot_sync(
-                        wmask, lane + k < 32 && jl < cnt && ((smask[jl] >> warp) & 1u));
+                        wmask, lane + k < 32 && jl < cnt && ((bmask[jl] >> warp) & 1u));
                     hits |= b << k;
                 }
                 while (hits) {
                     const int j = c0 + __ffs(hits) - 1;
                     hits &= hits - 1;
                     if (done) continue;
-                    const S s = sp[j];
-                    const Real dx = fx - s.mx;
-                    const Real dy = fy - s.my;
-                    const Real pw = half * (s.ca * dx * dx + s.cc * dy * dy) - s.cb * dx * dy;
+                    const S s = bsp[j];
+                    Real mx, my, ca, cb, cc, al;
+                    fields(s, mx, my, ca, cb, cc, al);
+                    const Real dx = fx - mx;
+                    const Real dy = fy - my;
+                    const Real pw = half * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
                     if (pw > (Real)0 || pw < skip_lo) continue;
-                    const Real ai = s.alpha * splat_exp(pw, s_tab);
+                    const Real ai = al * splat_exp(pw, s_tab);
                     if (ai < floor_a) continue;
+                    Real r, g, b;
+                    colours(s, r, g, b);
                     const Real w = ai * T;
-                    ar = ar + s.r * w;
-                    ag = ag + s.g * w;
-                    ab = ab + s.b * w;
+                    ar = ar + r * w;
+                    ag = ag + g * w;
+                    ab = ab + b * w;
                     aa = aa + w;
                     T = T * (one - ai);
                     last = (int)(b0 - lo) + j + 1;
@@ -172,6 +243,9 @@ __global__ void k_composite(ViewParams vp, const typename Px<Real>::Payload *__r
                 }
             }
         }
+        // the other buffer was last read in the previous batch (fenced by the
+        // barrier that ended it), so the prefetched splat can land there now
+        stage(b0 + nb, buf ^ 1, pre, have1);
         if (__syncthreads_count(!done) == 0) break;
     }
     if (inside) {
@@ -304,30 +378,31 @@ int launch_pack_payload(int64_t m, int precision, const void *means2d, const voi
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
-int launch_composite(const ViewParams &vp, const void *payload, const unsigned *vals0,
-                     const unsigned *vals1, const long long *sel, const int64_t *tile_starts,
-                     void *image, void *final_t, int32_t *last_contrib, cudaStream_t st) {
+int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
+    if (b.nviews == 0) return G6R_OK;
+    const ViewParams &vp = b.vp[0];
     const int threads = vp.tile_size * vp.tile_size;
-    const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
-    if (grid == 0) return G6R_OK;
-    static bool attrs_set = false;   // >48 KB dynamic smem for 32x32 f64 tiles
+    const dim3 grid((unsigned)(vp.tiles_x * vp.tiles_y), (unsigned)b.nviews);
+    if (grid.x == 0) return G6R_OK;
+    const int srt = sorted ? 1 : 0;
+    static bool attrs_set = false;   // > 48 KB dynamic smem for large f64 tiles
     if (!attrs_set) {
-        cudaFuncSetAttribute(k_composite<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             1024 * (int)(sizeof(Px<double>::S) + 4));
-        cudaFuncSetAttribute(k_composite<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             1024 * (int)(sizeof(Px<float>::S) + 4));
+        cudaFuncSetAttribute(k_composite<double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * 1024 * (int)(sizeof(Px<double>::S) + 4));
+        cudaFuncSetAttribute(k_composite<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * 1024 * (int)(sizeof(Px<float>::S) + 4));
         attrs_set = true;
     }
     if (vp.precision) {
-        const size_t smem = threads * (sizeof(Px<double>::S) + sizeof(unsigned));
-        k_composite<double><<<grid, threads, smem, st>>>(vp, (const PayloadF64 *)payload, vals0, vals1, sel,
-                                                         tile_starts, (double *)image,
-                                                         (double *)final_t, last_contrib);
+        if (vp.tile_size == 16)
+            k_composite<double, 256><<<grid, 256, 0, st>>>(b, srt);
+        else
+            k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
-        const size_t smem = threads * (sizeof(Px<float>::S) + sizeof(unsigned));
-        k_composite<float><<<grid, threads, smem, st>>>(vp, (const PayloadF32 *)payload, vals0, vals1, sel,
-                                                        tile_starts, (float *)image,
-                                                        (float *)final_t, last_contrib);
+        if (vp.tile_size == 16)
+            k_composite<float, 256><<<grid, 256, 0, st>>>(b, srt);
+        else
+            k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }

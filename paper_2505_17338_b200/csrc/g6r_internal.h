@@ -1,4 +1,10 @@
 // g6r_internal.h -- host-side launchers shared between the .cu translation units.
+//
+// Every per-view stage is launched for a *batch* of up to kMaxBatch views of
+// one scene at once (grid = work x views): a launch then always has enough
+// CTAs to fill the machine, a view's long tile runs overlap other views' work
+// inside one kernel instead of across streams, and the projection's record
+// stream is shared by the batch through L2.
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -8,15 +14,17 @@
 
 namespace g6r {
 
+constexpr int kMaxBatch = 8;
+
 // Workspace carve-up for one view (see g6r_api.cu::layout).
 struct Workspace {
-    long long *internal;            // kNumInternal int64 (tickets)
-    unsigned long long *proj_agg_m, *proj_agg_e, *proj_inc_m, *proj_inc_e;  // lookback, per projection block
+    long long *internal;            // kNumInternal int64 (tickets, depth extrema, passes)
+    unsigned long long *proj_status;   // look-back words, one per projection CTA
     void *payload;                  // n compositing payloads (f32 or f64)
     unsigned long long *keys[2];    // entry keys, ping-pong
     unsigned *vals[2];              // entry values (splat index), ping-pong
-    unsigned *hist;                 // kMaxPasses x kBins digit counts
-    unsigned *sort_status;          // kMaxPasses x tiles_cap x kBins lookback words
+    unsigned *hist;                 // kMaxPasses x kBins digit totals
+    unsigned *sort_counts;          // kMaxPasses x tiles_cap x kBins per-tile digit counts
     int64_t *tile_starts;           // T+1 (internal copy)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
@@ -30,6 +38,23 @@ struct ViewParams {
     int32_t iw, ih, tile_size, tiles_x, tiles_y, precision;
 };
 
+struct ViewOut {
+    void *image;
+    void *final_t;           // may be NULL
+    int32_t *last_contrib;   // may be NULL
+    int64_t *counters;       // G6R_NCOUNTERS
+    int32_t *entry_splat;    // optional copy of the sorted runs
+    int64_t *tile_starts;    // optional copy of the tile ranges
+};
+
+// One launch's views.  All views share tile size, precision and image size.
+struct Batch {
+    int nviews;
+    ViewParams vp[kMaxBatch];
+    Workspace ws[kMaxBatch];
+    ViewOut out[kMaxBatch];
+};
+
 int launch_prepare(int64_t n, const double *mu_p, const double *mu_d, const double *cov_raw,
                    const double *sh, const double *opacity_raw, const uint8_t *labels,
                    const double *ss, double ds, int w_mode, double *records, uint8_t *flags,
@@ -39,26 +64,25 @@ int launch_pack_records(int64_t n, const double *mu_p, const double *mu_d, const
                         const double *prec, const double *sigma_prime, const uint8_t *degenerate,
                         const uint8_t *labels, double *records, uint8_t *flags, cudaStream_t st);
 
-// fused slice+project+compact+duplicate; writes counters[M,E,fate,overflow]
-int launch_project(const g6r_scene &scene, uint32_t mask, const ViewParams &vp,
-                   const Workspace &ws, int64_t *counters, const g6r_splat_out *splats,
-                   bool write_entries, cudaStream_t st);
-// binning of external splats (count, scan, duplicate) into ws.keys[0]/vals[0]
+// zero every view's per-view scratch region (first clear_bytes of each workspace)
+// and its counters
+int launch_clear(const Batch &b, size_t clear_bytes, cudaStream_t st);
+// fused slice+project+compact+duplicate; writes counters[M,E,fate,overflow].
+// splats (SplatBatch-shaped outputs) only for single-view batches.
+int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
+                   const g6r_splat_out *splats, bool write_entries, cudaStream_t st);
+// binning of external splats (count, scan, duplicate) into ws.keys[0]/vals[0] (one view)
 int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, const double *depths,
-                     const ViewParams &vp, const Workspace &ws, int64_t *counters, cudaStream_t st);
-// radix sort of ws.keys[0]/vals[0] (E read from counters); *final_buf receives
-// the index (0/1) of the buffer holding the sorted result.
-int launch_sort(const ViewParams &vp, const Workspace &ws, const int64_t *counters, cudaStream_t st);
+                     const Batch &b, cudaStream_t st);
+// radix sort of every view's ws.keys[0]/vals[0] (E read from its counters)
+int launch_sort(const Batch &b, cudaStream_t st);
 // per-tile ranges into ws.tile_starts (+ optional copies of starts / entry_splat)
-int launch_ranges(const ViewParams &vp, const Workspace &ws, const int64_t *counters,
-                  int64_t *tile_starts_out, int32_t *entry_splat_out, cudaStream_t st);
+int launch_ranges(const Batch &b, cudaStream_t st);
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st);
 int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
                         const void *colors, const void *alphas, void *payload, cudaStream_t st);
-// entry values: vals0, or (sel != NULL) the sorted ping-pong buffer sel picks
-int launch_composite(const ViewParams &vp, const void *payload, const unsigned *vals0,
-                     const unsigned *vals1, const long long *sel, const int64_t *tile_starts, void *image, void *final_t,
-                     int32_t *last_contrib, cudaStream_t st);
+// sorted: entry values are the view's sorted ping-pong buffer; otherwise vals[0] holds them
+int launch_composite(const Batch &b, bool sorted, cudaStream_t st);
 int launch_composite_backward(int64_t m, const double *means2d, const double *conics,
                               const double *colors, const double *alphas,
                               const int32_t *entry_splat, const int64_t *tile_starts,
@@ -75,6 +99,6 @@ int launch_stage2(int64_t n, const double *view, const double *mean_adj, const d
                   double sh_c1, double *means2d, double *conics, double *colors, double *depths,
                   int32_t *radii, uint8_t *stage, cudaStream_t st);
 
-int sort_passes(int tiles);   // 8-bit LSD passes over (tile << 32 | depth32)
+int sort_passes(int tiles);   // upper bound on radix passes for `tiles` tiles
 
 }  // namespace g6r

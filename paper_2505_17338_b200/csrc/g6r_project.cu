@@ -8,9 +8,10 @@
 //   raster.py:340-375  bin_splats up to the key build (rects, counts, offsets,
 //                      duplication in splat order, key = tile<<32 | f32 depth)
 // One thread per Gaussian reads its 352-byte prepared record as 22 coalesced
-// 16-byte column loads (loaded lazily: culled rows stop early).  The compaction
-// index and the entry offset come from one decoupled-lookback scan across
-// CTAs, so the whole stage is a single launch with no host round trip.  All
+// 16-byte column loads, all issued up front.  A launch covers a batch of views
+// (grid = views x Gaussian blocks).  The compaction index and the entry offset
+// come from one decoupled-lookback scan across CTAs, so the whole stage is a
+// single launch with no host round trip.  All
 // arithmetic is IEEE double with the reference's association (-fmad=false);
 // the only transcendental, exp(-q/2), is CUDA's correctly-rounded-to-1ulp exp.
 #include "g6r_common.cuh"
@@ -168,7 +169,7 @@ __device__ __forceinline__ void lookback2(int64_t tile, long long bm, long long 
                                           long long *s_pe) {
     const int lane = threadIdx.x & 31;
     if (threadIdx.x >= 32) return;
-    unsigned long long *status = ws.proj_inc_m;
+    unsigned long long *status = ws.proj_status;
     if (tile == 0) {
         if (lane == 0) {
             st_volatile_u64(status, pack_status(kIncFlag, bm, be));
@@ -261,42 +262,80 @@ __device__ __forceinline__ void block_scan2(int a, int b, int &ea, int &eb, int 
     tot_b = s_wb[32];
 }
 
+// Per-CTA staging of the kept splats' tile rectangles for the duplication.
+struct EmitSmem {
+    int eoff[kBlock];   // exclusive entry offset inside the CTA
+    int x0[kBlock], y0[kBlock], wx[kBlock];
+    float rwx[kBlock];  // 1 / wx, for a division-free row/column split
+    unsigned db[kBlock];   // f32 depth bits
+};
+
+__device__ __forceinline__ void stage_rect(EmitSmem &es, int l, int eoff, int x0, int y0, int wx,
+                                           unsigned db) {
+    es.eoff[l] = eoff;
+    es.x0[l] = x0;
+    es.y0[l] = y0;
+    es.wx[l] = wx;
+    es.rwx[l] = 1.0f / (float)wx;
+    es.db[l] = db;
+}
+
 // Cooperative duplication of this CTA's kept splats into (key, value) entries,
 // in ascending splat order with tiles row-major inside each rect (the order
-// np.repeat produces in raster.py:369-375).
+// np.repeat produces in raster.py:369-375).  Entry j of the CTA belongs to the
+// largest l with eoff[l] <= j (binary search); the row/column split uses a
+// float reciprocal corrected to the exact integer quotient.
 __device__ __forceinline__ void emit_entries(int nk, int ne, long long m_base, long long e_base,
-                                             const int *s_eoff, const int *s_x0, const int *s_y0,
-                                             const int *s_wx, const unsigned *s_db,
-                                             const ViewParams &vp, unsigned long long *keys,
-                                             unsigned *vals) {
+                                             const EmitSmem &es, int tiles_x,
+                                             unsigned long long *keys, unsigned *vals) {
     for (int j = threadIdx.x; j < ne; j += blockDim.x) {
-        int lo = 0, hi = nk - 1;   // largest l with s_eoff[l] <= j
+        int lo = 0, hi = nk - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (s_eoff[mid] <= j) lo = mid;
+            if (es.eoff[mid] <= j) lo = mid;
             else hi = mid - 1;
         }
-        const int loc = j - s_eoff[lo];
-        const int w = s_wx[lo];
-        const int ty = s_y0[lo] + loc / w;
-        const int tx = s_x0[lo] + loc % w;
-        const unsigned long long tile = (unsigned long long)ty * (unsigned)vp.tiles_x + (unsigned)tx;
-        keys[e_base + j] = (tile << 32) | s_db[lo];
+        const int loc = j - es.eoff[lo];
+        const int w = es.wx[lo];
+        int q = (int)((float)loc * es.rwx[lo]);
+        if (q * w > loc) --q;
+        else if ((q + 1) * w <= loc) ++q;
+        const int ty = es.y0[lo] + q;
+        const int tx = es.x0[lo] + (loc - q * w);
+        const unsigned long long tile = (unsigned long long)ty * (unsigned)tiles_x + (unsigned)tx;
+        keys[e_base + j] = (tile << 32) | es.db[lo];
         vals[e_base + j] = (unsigned)(m_base + lo);
     }
 }
 
+// Reduce a CTA's drawn-splat depth bits into the view's extrema (for the radix
+// key compression in g6r_sort.cu).  Called by every thread.
+__device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *s_dext) {
+    const unsigned hi = __reduce_max_sync(0xffffffffu, kept ? db : 0u);
+    const unsigned lo_inv = __reduce_max_sync(0xffffffffu, kept ? ~db : 0u);
+    if ((threadIdx.x & 31) == 0 && hi) {
+        atomicMax(&s_dext[0], lo_inv);
+        atomicMax(&s_dext[1], hi);
+    }
+}
+
+// grid = (views, ceil(n / 256)): CTA (v, *) projects 256 Gaussians for view v.
+// The CTAs of the batch's views for one Gaussian block are adjacent in launch
+// order, so views 2..K read the block's records from L2.
 template <bool kF64>
 __global__ void __launch_bounds__(kBlock)
-k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *counters,
-          g6r_splat_out so, int write_entries, double sh_c0, double sh_c1) {
+k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_splat_out so,
+          int write_entries, double sh_c0, double sh_c1) {
     __shared__ int s_tile;
     __shared__ int s_wa[33], s_wb[33];
     __shared__ long long s_pm, s_pe;
     __shared__ unsigned s_fate[6];
-    __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
-    __shared__ unsigned s_db[kBlock];
+    __shared__ EmitSmem es;
     __shared__ unsigned s_dext[2];   // block max of ~depth_bits and of depth_bits
+    const int v = blockIdx.x;
+    const ViewParams &vp = b.vp[v];
+    const Workspace &ws = b.ws[v];
+    int64_t *counters = b.out[v].counters;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
     if (threadIdx.x < 6) s_fate[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
@@ -312,11 +351,11 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (i < n) {
         const unsigned fl = scene.flags[i];
         if (((mask >> (fl & 15u)) & 1u) && !(fl & G6R_FLAG_DEGENERATE)) {
-            // all 22 column packets issued at once: one HBM round trip per Gaussian
+            // all 22 column packets issued at once: one memory round trip per Gaussian
             double r[G6R_REC_DOUBLES];
 #pragma unroll
             for (int c = 0; c < G6R_REC_COLUMNS; ++c) {
-                const double2 q = __ldcs(&rec[c * n + i]);   // streamed once per view
+                const double2 q = __ldg(&rec[c * n + i]);
                 r[2 * c] = q.x;
                 r[2 * c + 1] = q.y;
             }
@@ -338,15 +377,8 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (st < 6) atomicAdd(&s_fate[st], 1u);
     const int kept = st == 0;
     const int cnt = kept ? wx * hy : 0;
-    {   // view depth-bit extrema for the radix key compression (g6r_sort.cu)
-        const unsigned db = kept ? __float_as_uint((float)o.depth) : 0u;
-        const unsigned hi = __reduce_max_sync(0xffffffffu, db);
-        const unsigned lo_inv = __reduce_max_sync(0xffffffffu, kept ? ~db : 0u);
-        if ((threadIdx.x & 31) == 0 && hi) {
-            atomicMax(&s_dext[0], lo_inv);
-            atomicMax(&s_dext[1], hi);
-        }
-    }
+    const unsigned db = kept ? __float_as_uint((float)o.depth) : 0u;
+    depth_extrema(kept, db, s_dext);
     int lm, le, bm, be;
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
     lookback2(tile, bm, be, ws, &s_pm, &s_pe);
@@ -368,7 +400,7 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
         } else {
             const float fa = (float)o.ca, fb = (float)o.cb, fc = (float)o.cc;
             float ex, ey;
-            cull_extents(fa, fb, fc, 0x1p-23, ex, ey);
+            cull_extents_f32(fa, fb, fc, ex, ey);
             PayloadF32 p;
             p.a = make_float4((float)o.u, (float)o.v, fa, fb);
             p.b = make_float4(fc, (float)o.alpha, (float)o.r, (float)o.g);
@@ -396,11 +428,7 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
             so.radii[2 * m] = o.rx;
             so.radii[2 * m + 1] = o.ry;
         }
-        s_eoff[lm] = le;
-        s_x0[lm] = x0;
-        s_y0[lm] = y0;
-        s_wx[lm] = wx;
-        s_db[lm] = __float_as_uint((float)o.depth);
+        stage_rect(es, lm, le, x0, y0, wx, db);
     }
     __syncthreads();
     if (threadIdx.x < 6 && s_fate[threadIdx.x])
@@ -409,28 +437,30 @@ k_project(g6r_scene scene, uint32_t mask, ViewParams vp, Workspace ws, int64_t *
     if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
     if (write_entries) {
         if (e_base + be <= ws.entry_capacity) {
-            emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0],
-                         ws.vals[0]);
+            emit_entries(bm, be, m_base, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
         } else if (threadIdx.x == 0) {
             counters[G6R_CNT_OVERFLOW] = 1;
         }
     }
-    if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+    if (tile == gridDim.y - 1 && threadIdx.x == 0) {
         counters[G6R_CNT_DRAWN] = m_base + bm;
         counters[G6R_CNT_ENTRIES] = e_base + be;
     }
 }
 
-// Binning of externally supplied splats (raster.py:340-375 on a given SplatBatch).
+// Binning of externally supplied splats (raster.py:340-375 on a given
+// SplatBatch), one view.
 __global__ void __launch_bounds__(kBlock)
 k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__restrict__ radii,
-            const double *__restrict__ depths, ViewParams vp, Workspace ws, int64_t *counters) {
+            const double *__restrict__ depths, const __grid_constant__ Batch b) {
     __shared__ int s_tile;
     __shared__ int s_wa[33], s_wb[33];
     __shared__ long long s_pm, s_pe;
-    __shared__ int s_eoff[kBlock], s_x0[kBlock], s_y0[kBlock], s_wx[kBlock];
-    __shared__ unsigned s_db[kBlock];
+    __shared__ EmitSmem es;
     __shared__ unsigned s_dext[2];
+    const ViewParams &vp = b.vp[0];
+    const Workspace &ws = b.ws[0];
+    int64_t *counters = b.out[0].counters;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
     if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
     __syncthreads();
@@ -440,31 +470,18 @@ k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__rest
     const int kept = i < m;
     if (kept) tile_rect(means2d[2 * i], means2d[2 * i + 1], radii[2 * i], radii[2 * i + 1], vp, x0, y0, wx, hy);
     const int cnt = kept ? wx * hy : 0;
-    {
-        const unsigned db = kept ? __float_as_uint((float)depths[i]) : 0u;
-        const unsigned hi = __reduce_max_sync(0xffffffffu, db);
-        const unsigned lo_inv = __reduce_max_sync(0xffffffffu, kept ? ~db : 0u);
-        if ((threadIdx.x & 31) == 0 && (hi | lo_inv)) {
-            atomicMax(&s_dext[0], lo_inv);
-            atomicMax(&s_dext[1], hi);
-        }
-    }
+    const unsigned db = kept ? __float_as_uint((float)depths[i]) : 0u;
+    depth_extrema(kept, db, s_dext);
     int lm, le, bm, be;
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
     lookback2(tile, bm, be, ws, &s_pm, &s_pe);
     __syncthreads();
-    if (kept) {
-        s_eoff[lm] = le;
-        s_x0[lm] = x0;
-        s_y0[lm] = y0;
-        s_wx[lm] = wx;
-        s_db[lm] = __float_as_uint((float)depths[i]);
-    }
+    if (kept) stage_rect(es, lm, le, x0, y0, wx, db);
     __syncthreads();
     if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
     const long long m_base = s_pm, e_base = s_pe;
     if (e_base + be <= ws.entry_capacity) {
-        emit_entries(bm, be, m_base, e_base, s_eoff, s_x0, s_y0, s_wx, s_db, vp, ws.keys[0], ws.vals[0]);
+        emit_entries(bm, be, m_base, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
     } else if (threadIdx.x == 0) {
         counters[G6R_CNT_OVERFLOW] = 1;
     }
@@ -523,27 +540,23 @@ __global__ void k_stage2(int64_t n, const double *view, const double *mean_adj, 
 static const double kShC0 = 0.28209479177387814;   // core.py:25
 static const double kShC1 = 0.4886025119029199;    // core.py:26
 
-int launch_project(const g6r_scene &scene, uint32_t mask, const ViewParams &vp,
-                   const Workspace &ws, int64_t *counters, const g6r_splat_out *splats,
-                   bool write_entries, cudaStream_t st) {
+int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
+                   const g6r_splat_out *splats, bool write_entries, cudaStream_t st) {
     g6r_splat_out so{};
     if (splats) so = *splats;
-    if (scene.n == 0) return G6R_OK;
-    const unsigned grid = (unsigned)ceil_div(scene.n, kBlock);
-    if (vp.precision)
-        k_project<true><<<grid, kBlock, 0, st>>>(scene, mask, vp, ws, counters, so, write_entries,
-                                                  kShC0, kShC1);
+    if (scene.n == 0 || b.nviews == 0) return G6R_OK;
+    const dim3 grid((unsigned)b.nviews, (unsigned)ceil_div(scene.n, kBlock));
+    if (b.vp[0].precision)
+        k_project<true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else
-        k_project<false><<<grid, kBlock, 0, st>>>(scene, mask, vp, ws, counters, so, write_entries,
-                                                   kShC0, kShC1);
+        k_project<false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
 int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, const double *depths,
-                     const ViewParams &vp, const Workspace &ws, int64_t *counters, cudaStream_t st) {
+                     const Batch &b, cudaStream_t st) {
     if (m == 0) return G6R_OK;
-    k_duplicate<<<(unsigned)ceil_div(m, kBlock), kBlock, 0, st>>>(m, means2d, radii, depths, vp, ws,
-                                                                   counters);
+    k_duplicate<<<(unsigned)ceil_div(m, kBlock), kBlock, 0, st>>>(m, means2d, radii, depths, b);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
