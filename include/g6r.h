@@ -185,6 +185,12 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask,
                      int64_t entry_capacity, const g6r_frame *frames /* host array */,
                      int32_t batch, g6r_profiler *prof, g6r_stream_t stream);
 
+/* Launch trace: with G6R_TRACE=1 in the environment every kernel launch is
+ * followed by a CUDA event; this writes "label,ms" rows (device time between
+ * consecutive launches' completions) to `path` (stderr if NULL) and clears the
+ * trace.  Synchronises on the last event. */
+int g6r_trace_dump(const char *path);
+
 /* Test probe: y[i] = the device expf used by the f32 compositor (glibc
  * algorithm, g6r_common.cuh) for n floats. */
 int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream);

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <string>
 
 #include "g6r_common.cuh"
@@ -159,7 +161,34 @@ int launch_clear(const Batch &b, size_t clear_bytes, cudaStream_t st) {
     const size_t words = clear_bytes / 8;
     const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>((words + 255) / 256, 64));
     k_clear<<<dim3(gx, b.nviews), 256, 0, st>>>(b, words);
+    trace_mark("clear", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+// --- launch trace -----------------------------------------------------------
+struct TraceRec {
+    const char *label;
+    cudaEvent_t ev;
+};
+static std::mutex g_trace_mu;
+static std::vector<TraceRec> g_trace;
+static int g_trace_on = -1;
+
+static bool trace_enabled() {
+    if (g_trace_on < 0) {
+        const char *e = getenv("G6R_TRACE");
+        g_trace_on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return g_trace_on == 1;
+}
+
+void trace_mark(const char *label, cudaStream_t st) {
+    if (!trace_enabled()) return;
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return;
+    cudaEventRecord(ev, st);
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    g_trace.push_back(TraceRec{label, ev});
 }
 
 }  // namespace g6r
@@ -339,6 +368,24 @@ int g6r_profiler_read(g6r_profiler *p, double *stage_ms, int32_t *views) {
             stage_ms[s] += ms;
         }
     return cuda_check("profiler read");
+}
+
+int g6r_trace_dump(const char *path) {
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    if (g_trace.empty()) return G6R_OK;
+    cudaEventSynchronize(g_trace.back().ev);
+    FILE *f = path ? fopen(path, "w") : stderr;
+    if (!f) return fail(G6R_EINVAL, "cannot open %s", path);
+    fprintf(f, "label,ms_since_previous_mark\n");
+    for (size_t i = 1; i < g_trace.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_trace[i - 1].ev, g_trace[i].ev);
+        fprintf(f, "%s,%.4f\n", g_trace[i].label, ms);
+    }
+    if (path) fclose(f);
+    for (auto &r : g_trace) cudaEventDestroy(r.ev);
+    g_trace.clear();
+    return cuda_check("trace dump");
 }
 
 int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream) {

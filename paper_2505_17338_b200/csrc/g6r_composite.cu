@@ -404,6 +404,7 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         else
             k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
     }
+    trace_mark("composite", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 

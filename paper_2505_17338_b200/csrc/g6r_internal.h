@@ -101,4 +101,10 @@ int launch_stage2(int64_t n, const double *view, const double *mean_adj, const d
 
 int sort_passes(int tiles);   // upper bound on radix passes for `tiles` tiles
 
+// Launch trace (G6R_TRACE=1 in the environment): a CUDA event is recorded on
+// the stream after every kernel launch, labelled with the kernel; the C ABI's
+// g6r_trace_dump prints per-launch device intervals.  Off by default (one
+// branch per launch).
+void trace_mark(const char *label, cudaStream_t st);
+
 }  // namespace g6r

@@ -550,6 +550,7 @@ int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
         k_project<true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else
         k_project<false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    trace_mark("project", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 

@@ -313,8 +313,11 @@ int launch_sort(const Batch &b, cudaStream_t st) {
         1, std::min<int64_t>(tiles_cap, std::max<int64_t>(sms * 8 / b.nviews, 1)));
     for (int p = 0; p < max_passes; ++p) {
         k_upsweep<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b, tbits, p);
+        trace_mark("upsweep", st);
         k_colscan<<<dim3(kBins / 32, b.nviews), kBlock, 0, st>>>(b, tbits, p);
+        trace_mark("colscan", st);
         k_downsweep<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b, tbits, p);
+        trace_mark("downsweep", st);
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
@@ -325,6 +328,7 @@ int launch_ranges(const Batch &b, cudaStream_t st) {
     const unsigned gx = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(cap + 1, kBlock), std::max(num_sms() * 4 / b.nviews, 1)));
     k_ranges<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b);
+    trace_mark("ranges", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 

@@ -506,7 +506,7 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
     return _launch(prep, bits, camera, config, False, int(capacity or prep.entry_hint))
 
 
-DEFAULT_CONCURRENCY = 4
+DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
 
 
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
@@ -546,6 +546,52 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     return images, counters
 
 
+def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
+                 batch: int = DEFAULT_CONCURRENCY) -> np.ndarray:
+    """Render many views to host memory: (V, H, W, 4) like stacking
+    ``render(scene, cam)`` over ``cameras``.
+
+    Views are rendered ``batch`` per launch on the current stream; each chunk's
+    images are copied device->host into pinned memory on a side stream while
+    the next chunk renders.  One synchronisation at the end; views that
+    overflowed the entry capacity are re-rendered individually."""
+    prep = prepare_scene(scene, config.w_mode)
+    bits = _selection(prep, group_mask, config, RenderStats())
+    cams = list(cameras)
+    V = len(cams)
+    if V == 0:
+        return np.zeros((0, 0, 0, 4), dtype=config.dtype())
+    H, W = int(cams[0].height), int(cams[0].width)
+    dt = torch.float32 if config.precision == "f32" else torch.float64
+    dev = prep.device
+    images = torch.empty((V, H, W, 4), dtype=dt, device=dev)
+    # pinned output owned by the returned array (torch's caching host allocator
+    # recycles the block once the array is released): no extra host copy
+    host = torch.empty((V, H, W, 4), dtype=dt, pin_memory=True)
+    main = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    counters = []
+    chunk = max(1, min(int(batch), 8))
+    for k in range(0, V, chunk):
+        sl = slice(k, min(V, k + chunk))
+        _, cnt = render_views(scene, cams[sl], group_mask, config, out=images[sl],
+                              concurrency=chunk)
+        counters.append(cnt)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        copy.wait_event(ev)
+        with torch.cuda.stream(copy):
+            host[sl].copy_(images[sl], non_blocking=True)
+            images[sl].record_stream(copy)
+    copy.synchronize()
+    cnt = torch.cat(counters).cpu().numpy()
+    out = host.numpy()
+    for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
+        fr, _ = _render_checked(prep, bits, cams[v], config, False)
+        out[v] = fr.image.cpu().numpy()
+    return out
+
+
 def _stats_from_counters(stats: RenderStats, counters) -> None:
     fate = counters[nat.CNT_FATE:nat.CNT_FATE + 6]
     stats.n_view_degenerate = int(fate[1])
@@ -583,8 +629,18 @@ def render(scene, camera, group_mask=None, config: RenderConfig = DEFAULT_CONFIG
     """(H, W, 4) premultiplied RGBA (raster.py:458-466)."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
-    fr, _ = _render_checked(prep, bits, camera, config, False)
-    return fr.image.cpu().numpy()
+    while True:
+        fr = _launch(prep, bits, camera, config, False, int(prep.entry_hint))
+        # image and counters come back in one synchronisation, via pinned memory
+        img = torch.empty(fr.image.shape, dtype=fr.image.dtype, pin_memory=True)
+        cnt = torch.empty(nat.NCOUNTERS, dtype=torch.int64, pin_memory=True)
+        img.copy_(fr.image, non_blocking=True)
+        cnt.copy_(fr.counters, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        c = cnt.numpy()
+        if not c[nat.CNT_OVERFLOW]:
+            return img.numpy()
+        prep.entry_hint = min(int(c[nat.CNT_ENTRIES] * 1.25) + 4096, (1 << 30) - 1)
 
 
 # ---------------------------------------------------------------------------
