@@ -238,6 +238,8 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     if (launch_project(*scene, mask, b, nviews == 1 ? splats : nullptr, true, st))
         return cuda_check("project");
     prof_mark(prof, 1, st);
+    // (Sorting the batch in L2-sized sub-batches was measured slower: the extra
+    //  launches cost more than the HBM traffic they save.)
     if (launch_sort(b, st)) return cuda_check("sort");
     prof_mark(prof, 2, st);
     if (launch_ranges(b, st)) return cuda_check("ranges");
