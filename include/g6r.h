@@ -185,6 +185,27 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask,
                      int64_t entry_capacity, const g6r_frame *frames /* host array */,
                      int32_t batch, g6r_profiler *prof, g6r_stream_t stream);
 
+/* Backward render (diffrender.py:401-439 render_backward): an f64 forward of
+ * the view followed by the adjoint compositor, the per-splat reduction and the
+ * chain to the raw parameters (diffrender.py:183-398).  grad_image is
+ * d loss / d image (H,W,4) f64; the gradient arrays (scene rows, shapes as the
+ * raw scene: (n,3) (n,3) (n,21) (n,12) (n)) are fully overwritten -- culled,
+ * masked and degenerate Gaussians get exact zeros.  cfg->precision must be 1
+ * and cfg->tile_size 16.  mu_p/mu_d/cov_raw/sh are the scene's raw device
+ * arrays (the factor L is rebuilt from cov_raw); spatial_scale is host (3).
+ * image_out (optional, (H,W,4) f64) receives the forward image.  Deterministic:
+ * no floating-point atomics. */
+size_t g6r_backward_workspace_bytes(int64_t n, int32_t width, int32_t height, int32_t tile_size,
+                                    int64_t entry_capacity);
+int g6r_render_backward(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
+                        const g6r_config *cfg, void *workspace, size_t workspace_bytes,
+                        int64_t entry_capacity, const double *mu_p, const double *mu_d,
+                        const double *cov_raw, const double *sh,
+                        const double *spatial_scale /* host (3) */, double directional_scale,
+                        int32_t w_mode, const double *grad_image, double *g_mu_p, double *g_mu_d,
+                        double *g_cov_raw, double *g_sh, double *g_opacity_raw, int64_t *counters,
+                        double *image_out, g6r_stream_t stream);
+
 /* Launch trace: with G6R_TRACE=1 in the environment every kernel launch is
  * followed by a CUDA event; this writes "label,ms" rows (device time between
  * consecutive launches' completions) to `path` (stderr if NULL) and clears the

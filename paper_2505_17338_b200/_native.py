@@ -91,6 +91,9 @@ _SIGS = {
     "g6r_profiler_read": (ctypes.c_int, [P, P, P]),
     "g6r_debug_expf": (ctypes.c_int, [I64, P, P, P]),
     "g6r_trace_dump": (ctypes.c_int, [ctypes.c_char_p]),
+    "g6r_backward_workspace_bytes": (SZ, [I64, I32, I32, I32, I64]),
+    "g6r_render_backward": (ctypes.c_int, [P, U32, P, P, P, SZ, I64, P, P, P, P, P, D, I32, P, P, P,
+                                           P, P, P, P, P, P]),
     "g6r_project": (ctypes.c_int, [P, U32, P, P, P, SZ, P, P, P]),
     "g6r_bin": (ctypes.c_int, [I64, P, P, P, I32, I32, I32, P, SZ, I64, P, P, P, P]),
     "g6r_composite": (ctypes.c_int, [I64, I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, P, SZ,

@@ -390,6 +390,94 @@ int g6r_trace_dump(const char *path) {
     return cuda_check("trace dump");
 }
 
+// Backward workspace: the f64 forward layout followed by the gradient buffers.
+struct BwdLayout {
+    size_t fwd, gids, rect, egrad, gsplat, final_t, last, image, total;
+};
+
+static BwdLayout bwd_layout(int64_t n, int32_t width, int32_t height, int32_t tile_size, int64_t cap) {
+    BwdLayout B{};
+    const int64_t tiles = (int64_t)((width + tile_size - 1) / tile_size) * ((height + tile_size - 1) / tile_size);
+    const int64_t hw = (int64_t)width * height;
+    const int64_t nn = n > 0 ? n : 1;
+    size_t o = layout(n, tiles, cap, 1).total;
+    B.fwd = 0;
+    B.gids = o;
+    o = align_up(o + nn * 8);
+    B.rect = o;
+    o = align_up(o + nn * 16);
+    B.egrad = o;
+    o = align_up(o + (size_t)(cap > 0 ? cap : 1) * 72);
+    B.gsplat = o;
+    o = align_up(o + nn * 72);
+    B.final_t = o;
+    o = align_up(o + hw * 8);
+    B.last = o;
+    o = align_up(o + hw * 4);
+    B.image = o;
+    o = align_up(o + hw * 32);
+    B.total = o;
+    return B;
+}
+
+size_t g6r_backward_workspace_bytes(int64_t n, int32_t width, int32_t height, int32_t tile_size,
+                                    int64_t entry_capacity) {
+    if (n < 0 || width < 1 || height < 1 || tile_size < 1) return 0;
+    return bwd_layout(n, width, height, tile_size, entry_capacity).total;
+}
+
+int g6r_render_backward(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
+                        const g6r_config *cfg, void *workspace, size_t workspace_bytes,
+                        int64_t entry_capacity, const double *mu_p, const double *mu_d,
+                        const double *cov_raw, const double *sh, const double *spatial_scale,
+                        double directional_scale, int32_t w_mode, const double *grad_image,
+                        double *g_mu_p, double *g_mu_d, double *g_cov_raw, double *g_sh,
+                        double *g_opacity_raw, int64_t *counters, double *image_out,
+                        g6r_stream_t stream) {
+    if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL");
+    if (int rc = check_config(cfg)) return rc;
+    if (cfg->precision != 1) return fail(G6R_EINVAL, "the backward pass runs in f64 (precision=1)");
+    if (cfg->tile_size != 16) return fail(G6R_EINVAL, "the backward kernel supports tile_size 16");
+    if (w_mode != 0 && w_mode != 1) return fail(G6R_EINVAL, "w_mode must be 0 or 1");
+    if (!spatial_scale || !counters || !grad_image) return fail(G6R_EINVAL, "NULL argument");
+    if (scene->n > 0 && (!mu_p || !mu_d || !cov_raw || !sh || !g_mu_p || !g_mu_d || !g_cov_raw ||
+                         !g_sh || !g_opacity_raw))
+        return fail(G6R_EINVAL, "NULL scene or gradient array");
+    if (int rc = check_cap(entry_capacity)) return rc;
+    ViewParams vp;
+    if (int rc = make_view(cam, cfg, vp)) return rc;
+    const BwdLayout B = bwd_layout(scene->n, vp.iw, vp.ih, vp.tile_size, entry_capacity);
+    if (int rc = check_ws(B.total, workspace, workspace_bytes)) return rc;
+    char *base = static_cast<char *>(workspace);
+    const int64_t tiles = (int64_t)vp.tiles_x * vp.tiles_y;
+    const Layout L = layout(scene->n, tiles, entry_capacity, 1);
+    Batch b;
+    memset(&b, 0, sizeof b);
+    b.nviews = 1;
+    b.vp[0] = vp;
+    b.ws[0] = carve(base, L, entry_capacity);
+    b.ws[0].splat_rect = reinterpret_cast<int4 *>(base + B.rect);
+    double *final_t = reinterpret_cast<double *>(base + B.final_t);
+    int32_t *last = reinterpret_cast<int32_t *>(base + B.last);
+    int64_t *gids = reinterpret_cast<int64_t *>(base + B.gids);
+    b.out[0] = ViewOut{image_out ? (void *)image_out : (void *)(base + B.image), final_t, last, counters, nullptr, nullptr};
+    g6r_splat_out so{};
+    so.gids = gids;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
+    if (launch_project(*scene, group_mask, b, &so, true, st)) return cuda_check("project");
+    if (launch_sort(b, st)) return cuda_check("sort");
+    if (launch_ranges(b, st)) return cuda_check("ranges");
+    if (launch_composite(b, true, st)) return cuda_check("composite");
+    const int rc = launch_backward(vp, *scene, b.ws[0], counters, final_t, last, grad_image, gids,
+                                   reinterpret_cast<double *>(base + B.egrad),
+                                   reinterpret_cast<double *>(base + B.gsplat), mu_p, mu_d, cov_raw,
+                                   sh, spatial_scale, directional_scale, w_mode, g_mu_p, g_mu_d,
+                                   g_cov_raw, g_sh, g_opacity_raw, st);
+    if (rc) return rc == G6R_EINVAL ? fail(rc, "backward: bad view") : cuda_check("backward");
+    return G6R_OK;
+}
+
 int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream) {
     if (n < 0) return fail(G6R_EINVAL, "n must be >= 0");
     if (launch_debug_expf(n, x, y, (cudaStream_t)stream)) return cuda_check("debug_expf");

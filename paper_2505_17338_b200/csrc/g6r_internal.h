@@ -26,6 +26,7 @@ struct Workspace {
     unsigned *hist;                 // kMaxPasses x kBins digit totals
     unsigned *sort_counts;          // kMaxPasses x tiles_cap x kBins per-tile digit counts
     int64_t *tile_starts;           // T+1 (internal copy)
+    int4 *splat_rect;               // optional (backward): per splat (entry offset, x0, y0, wx)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
 };
@@ -98,6 +99,13 @@ int launch_stage2(int64_t n, const double *view, const double *mean_adj, const d
                   double lim_y, double width, double height, double low_pass, double sh_c0,
                   double sh_c1, double *means2d, double *conics, double *colors, double *depths,
                   int32_t *radii, uint8_t *stage, cudaStream_t st);
+
+int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspace &ws,
+                    const int64_t *counters, const double *final_t, const int32_t *last,
+                    const double *grad_image, const int64_t *gids, double *egrad, double *gsplat,
+                    const double *mu_p, const double *mu_d, const double *cov_raw, const double *sh,
+                    const double *ss, double ds, int w_mode, double *g_mu_p, double *g_mu_d,
+                    double *g_cov_raw, double *g_sh, double *g_opacity_raw, cudaStream_t st);
 
 int sort_passes(int tiles);   // upper bound on radix passes for `tiles` tiles
 

@@ -429,6 +429,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             so.radii[2 * m + 1] = o.ry;
         }
         stage_rect(es, lm, le, x0, y0, wx, db);
+        if (ws.splat_rect) ws.splat_rect[m] = make_int4((int)(e_base + le), x0, y0, wx);
     }
     __syncthreads();
     if (threadIdx.x < 6 && s_fate[threadIdx.x])

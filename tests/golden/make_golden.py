@@ -94,6 +94,32 @@ def make_case(name, seed, n, cam_kw, cfg_kw):
     print(name, "M", st.stats.n_drawn, "E", st.stats.n_entries)
 
 
+BACKWARD_CASES = ("rand40", "rand400", "rand400_raw", "cull100")
+
+
+def make_backward(name):
+    """Reference render_backward (diffrender.py:401-439) for a fixture scene and
+    a seeded d loss / d image."""
+    from splatct.diffrender import render_backward
+    z = np.load(os.path.join(HERE, f"{name}.npz"))
+    s = RefScene(mu_p=z["mu_p"], mu_d=z["mu_d"], cov_raw=z["cov_raw"], sh=z["sh"],
+                 opacity_raw=z["opacity_raw"], labels=z["labels"], spacing=np.ones(3),
+                 origin=np.zeros(3), direction=np.eye(3), spatial_scale=z["spatial_scale"],
+                 directional_scale=float(z["directional_scale"]))
+    from splatct.camera import Camera
+    w, h = (int(v) for v in z["cam_wh"])
+    cam = Camera(position=z["cam_position"], rotation=z["cam_rotation"], fov_y=float(z["cam_fov"]),
+                 width=w, height=h)
+    w_mode = "raw" if int(z["config"][1]) else "peak"
+    g = np.random.default_rng(1000 + len(name)).normal(size=(h, w, 4))
+    buf = render_backward(s, cam, g, None, raster.RenderConfig(precision="f64", w_mode=w_mode,
+                                                               threads=1))
+    np.savez_compressed(os.path.join(HERE, f"bwd_{name}.npz"), grad_image=g,
+                        **{f"g_{k}": getattr(buf, k) for k in
+                           ("mu_p", "mu_d", "cov_raw", "sh", "opacity_raw")})
+    print("bwd", name, float(np.abs(buf.cov_raw).max()))
+
+
 def make_expf():
     libm = ctypes.CDLL("libm.so.6")
     libm.expf.restype = ctypes.c_float
@@ -106,6 +132,10 @@ def make_expf():
 
 
 if __name__ == "__main__":
-    for case in CASES:
-        make_case(*case)
-    make_expf()
+    only_bwd = len(sys.argv) > 1 and sys.argv[1] == "backward"
+    if not only_bwd:
+        for case in CASES:
+            make_case(*case)
+        make_expf()
+    for name in BACKWARD_CASES:
+        make_backward(name)
