@@ -206,6 +206,58 @@ int g6r_render_backward(const g6r_scene *scene, uint32_t group_mask, const g6r_c
                         double *g_cov_raw, double *g_sh, double *g_opacity_raw, int64_t *counters,
                         double *image_out, g6r_stream_t stream);
 
+/* The two halves of g6r_render_backward, for loops that compute the loss
+ * between them (the fine-tune loop): the f64 forward keeps its state
+ * (sorted runs, final_t, last_contrib, splat rows) in the workspace and writes
+ * the image to image_out; apply then runs the adjoint on that state.  Both
+ * calls must see the same scene, camera, config and entry_capacity. */
+int g6r_backward_forward(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
+                         const g6r_config *cfg, void *workspace, size_t workspace_bytes,
+                         int64_t entry_capacity, int64_t *counters, double *image_out,
+                         g6r_stream_t stream);
+int g6r_backward_apply(const g6r_scene *scene, const g6r_camera *cam, const g6r_config *cfg,
+                       void *workspace, size_t workspace_bytes, int64_t entry_capacity,
+                       const double *mu_p, const double *mu_d, const double *cov_raw,
+                       const double *sh, const double *spatial_scale /* host (3) */,
+                       double directional_scale, int32_t w_mode, const double *grad_image,
+                       double *g_mu_p, double *g_mu_d, double *g_cov_raw, double *g_sh,
+                       double *g_opacity_raw, int64_t *counters, g6r_stream_t stream);
+
+/* Scene ingest (sceneio.py:77-111): decode `n` G6DS 168-byte records (the
+ * block after the 168-byte file header, already in device memory, 8-byte
+ * aligned) into the f64 SoA scene arrays (n,3) (n,3) (n,21) (n,12) (n) and
+ * labels (n).  Sets *bad (device int32) to 1 if any parameter is not finite or
+ * a label lies outside [1, 11]. */
+int g6r_decode_records(int64_t n, const void *records, double *mu_p, double *mu_d,
+                       double *cov_raw, double *sh, double *opacity_raw, uint8_t *labels,
+                       int32_t *bad, g6r_stream_t stream);
+
+/* Photometric loss lambda_l1 * L1 + lambda_ssim * (1 - MS-SSIM) on the RGB
+ * channels and its gradient with respect to the rendered image
+ * (diffrender.py:117-138 _loss_parts, _ssim.py:123-201 ms_ssim_with_grad).
+ * pred is (H,W,4) f64 on the device, target (H,W,target_channels) f64 with
+ * target_channels 3 or 4; grad_out (H,W,4) is fully written (alpha slot 0).
+ * weights (host, `scales` entries) are normalised here over the effective
+ * scale count; images under 2^(scales-1)*11 px per side use single-scale
+ * SSIM.  parts (host, 3) = {total, l1, ssim_loss}.  Synchronises the stream
+ * (the scalar reductions are read back).  Deterministic. */
+size_t g6r_loss_workspace_bytes(int32_t width, int32_t height);
+int g6r_loss_grad(const double *pred, const double *target, int32_t target_channels,
+                  int32_t width, int32_t height, double lambda_l1, double lambda_ssim,
+                  int32_t scales, const double *weights, void *workspace, size_t workspace_bytes,
+                  double *grad_out, double *parts, g6r_stream_t stream);
+
+/* One bias-corrected Adam update of `count` f64 parameters in place
+ * (diffrender.py:481-509, betas 0.9/0.999, eps 1e-8, the reference's operation
+ * order): m, v are the moment buffers; lr is this group's learning rate;
+ * bias1 = 1 - 0.9^t, bias2 = 1 - 0.999^t. */
+int g6r_adam_step(int64_t count, double *param, const double *grad, double *m, double *v,
+                  double lr, double bias1, double bias2, g6r_stream_t stream);
+
+/* Sets *flag (device int32) to 1 if any of `count` doubles is not finite;
+ * leaves it unchanged otherwise (GradientBuffer.all_finite, diffrender.py:179). */
+int g6r_any_nonfinite(int64_t count, const double *x, int32_t *flag, g6r_stream_t stream);
+
 /* Launch trace: with G6R_TRACE=1 in the environment every kernel launch is
  * followed by a CUDA event; this writes "label,ms" rows (device time between
  * consecutive launches' completions) to `path` (stderr if NULL) and clears the

@@ -389,3 +389,124 @@ def psnr(a, b):
     d = np.asarray(a, np.float64)[..., :3] - np.asarray(b, np.float64)[..., :3]
     mse = float(np.mean(d * d))
     return float("inf") if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
+
+
+# ---------------------------------------------------------------------------
+# Photometric loss of the fine-tune loop (diffrender.py:117-138) and the
+# multi-scale SSIM it uses (_ssim.py:23-201), restated with shifted-slice
+# accumulation instead of sliding-window einsums.
+# ---------------------------------------------------------------------------
+
+_SSIM_C1 = 0.01 ** 2
+_SSIM_C2 = 0.03 ** 2
+
+
+def ssim_window(size=11, sigma=1.5):
+    """_ssim.py:23-30: normalised 1-D Gaussian, centre (size-1)/2."""
+    x = np.arange(size) - (size - 1) / 2.0
+    g = np.exp(-(x ** 2) / (2.0 * sigma ** 2))
+    return g / g.sum()
+
+
+def _corr(img, w, full=False):
+    """Separable 2-D correlation, valid (or full = the adjoint) (_ssim.py:33-51)."""
+    k = len(w)
+    if full:
+        img = np.pad(img, k - 1)
+    h = img.shape[0] - k + 1
+    t = sum(w[i] * img[i:i + h] for i in range(k))
+    wv = img.shape[1] - k + 1
+    return sum(w[i] * t[:, i:i + wv] for i in range(k))
+
+
+def _pool(img):
+    h2, w2 = img.shape[0] // 2, img.shape[1] // 2
+    v = img[:2 * h2, :2 * w2]
+    return 0.25 * (v[0::2, 0::2] + v[1::2, 0::2] + v[0::2, 1::2] + v[1::2, 1::2])
+
+
+def _pool_adjoint(g, shape):
+    out = np.zeros(shape)
+    h2, w2 = g.shape
+    out[:2 * h2, :2 * w2] = 0.25 * np.repeat(np.repeat(g, 2, axis=0), 2, axis=1)
+    return out
+
+
+def _ssim_level(x, y, w):
+    ux, uy = _corr(x, w), _corr(y, w)
+    sxx = _corr(x * x, w) - ux * ux
+    syy = _corr(y * y, w) - uy * uy
+    sxy = _corr(x * y, w) - ux * uy
+    b1 = ux * ux + uy * uy + _SSIM_C1
+    b2 = sxx + syy + _SSIM_C2
+    return dict(x=x, y=y, ux=ux, uy=uy, b1=b1, b2=b2, l=(2.0 * ux * uy + _SSIM_C1) / b1,
+                cs=(2.0 * sxy + _SSIM_C2) / b2)
+
+
+def _ssim_level_backward(p, g_lcs, g_cs, w):
+    """_ssim.py:86-98 with scalar per-window upstream gradients."""
+    g_l = g_lcs * p["cs"]
+    g_t = g_lcs * p["l"] + g_cs
+    g_ux = (g_l * 2.0 * (p["uy"] - p["l"] * p["ux"]) / p["b1"]
+            + g_t * 2.0 * (p["cs"] * p["ux"] - p["uy"]) / p["b2"])
+    g_exx = -g_t * p["cs"] / p["b2"]
+    g_exy = g_t * 2.0 / p["b2"]
+    return (_corr(g_ux, w, True) + 2.0 * p["x"] * _corr(g_exx, w, True)
+            + p["y"] * _corr(g_exy, w, True))
+
+
+def ms_ssim_with_grad(a, b, scales=5, weights=(0.0448, 0.2856, 0.3001, 0.2363, 0.1333)):
+    """Value and d/da of MS-SSIM over the channels of (H,W,C) images (_ssim.py:123-201)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    w = ssim_window()
+    ns = 1 if min(a.shape[:2]) < (2 ** (scales - 1)) * 11 else scales
+    wt = np.asarray(weights[:ns], np.float64)
+    wt = wt / wt.sum()
+    total, grad = 0.0, np.zeros(a.shape)
+    for c in range(a.shape[2]):
+        x, y, lv = a[:, :, c], b[:, :, c], []
+        for j in range(ns):
+            lv.append(_ssim_level(x, y, w))
+            if j + 1 < ns:
+                x, y = _pool(x), _pool(y)
+        if ns == 1:
+            p = lv[0]
+            value = float(np.mean(p["l"] * p["cs"]))
+            g = _ssim_level_backward(p, 1.0 / p["cs"].size, 0.0, w)
+        else:
+            terms = [max(float(np.mean(p["l"] * p["cs"])) if j == ns - 1 else
+                         float(np.mean(p["cs"])), 0.0) for j, p in enumerate(lv)]
+            value = float(np.prod(np.power(terms, wt)))
+            g = np.zeros(lv[-1]["x"].shape)
+            for j in range(ns - 1, -1, -1):
+                p = lv[j]
+                if j < ns - 1:
+                    g = _pool_adjoint(g, p["x"].shape)
+                if value > 0.0 and terms[j] > 0.0:
+                    per = value * wt[j] / terms[j] / p["cs"].size
+                    g = g + (_ssim_level_backward(p, per, 0.0, w) if j == ns - 1
+                             else _ssim_level_backward(p, 0.0, per, w))
+        total += value
+        grad[:, :, c] = g
+    n = a.shape[2]
+    return total / n, grad / n
+
+
+def loss_parts(pred, gt, lambda_l1=0.8, lambda_ssim=0.2, scales=5,
+               weights=(0.0448, 0.2856, 0.3001, 0.2363, 0.1333)):
+    """(total, l1, ssim_loss, d total / d pred) over RGB (diffrender.py:117-138)."""
+    pred = np.asarray(pred, np.float64)
+    p, g = pred[:, :, :3], np.asarray(gt, np.float64)[:, :, :3]
+    d = p - g
+    l1 = float(np.mean(np.abs(d)))
+    grad = np.zeros(pred.shape)
+    grad_rgb = lambda_l1 * np.sign(d) / d.size
+    ssim_loss = 0.0
+    if lambda_ssim > 0.0:
+        wts = np.asarray(weights, np.float64)
+        value, gm = ms_ssim_with_grad(p, g, scales, wts / wts.sum())
+        ssim_loss = 1.0 - value
+        grad_rgb = grad_rgb - lambda_ssim * gm
+    grad[:, :, :3] = grad_rgb
+    return lambda_l1 * l1 + lambda_ssim * ssim_loss, l1, ssim_loss, grad

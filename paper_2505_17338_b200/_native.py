@@ -94,6 +94,14 @@ _SIGS = {
     "g6r_backward_workspace_bytes": (SZ, [I64, I32, I32, I32, I64]),
     "g6r_render_backward": (ctypes.c_int, [P, U32, P, P, P, SZ, I64, P, P, P, P, P, D, I32, P, P, P,
                                            P, P, P, P, P, P]),
+    "g6r_backward_forward": (ctypes.c_int, [P, U32, P, P, P, SZ, I64, P, P, P]),
+    "g6r_backward_apply": (ctypes.c_int, [P, P, P, P, SZ, I64, P, P, P, P, P, D, I32, P, P, P, P,
+                                          P, P, P, P]),
+    "g6r_decode_records": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
+    "g6r_loss_workspace_bytes": (SZ, [I32, I32]),
+    "g6r_loss_grad": (ctypes.c_int, [P, P, I32, I32, I32, D, D, I32, P, P, SZ, P, P, P]),
+    "g6r_adam_step": (ctypes.c_int, [I64, P, P, P, P, D, D, D, P]),
+    "g6r_any_nonfinite": (ctypes.c_int, [I64, P, P, P]),
     "g6r_project": (ctypes.c_int, [P, U32, P, P, P, SZ, P, P, P]),
     "g6r_bin": (ctypes.c_int, [I64, P, P, P, I32, I32, I32, P, SZ, I64, P, P, P, P]),
     "g6r_composite": (ctypes.c_int, [I64, I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, P, SZ,

@@ -426,6 +426,84 @@ size_t g6r_backward_workspace_bytes(int64_t n, int32_t width, int32_t height, in
     return bwd_layout(n, width, height, tile_size, entry_capacity).total;
 }
 
+// Validate and carve a backward workspace (shared by the forward-with-state
+// and apply halves, which must see the same scene, camera and capacity).
+static int bwd_setup(const g6r_scene *scene, const g6r_camera *cam, const g6r_config *cfg,
+                     void *workspace, size_t workspace_bytes, int64_t cap, int64_t *counters,
+                     double *image_out, Batch &b, BwdLayout &B) {
+    if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL");
+    if (int rc = check_config(cfg)) return rc;
+    if (cfg->precision != 1) return fail(G6R_EINVAL, "the backward pass runs in f64 (precision=1)");
+    if (cfg->tile_size != 16) return fail(G6R_EINVAL, "the backward kernel supports tile_size 16");
+    if (!counters) return fail(G6R_EINVAL, "counters are required");
+    if (int rc = check_cap(cap)) return rc;
+    ViewParams vp;
+    if (int rc = make_view(cam, cfg, vp)) return rc;
+    B = bwd_layout(scene->n, vp.iw, vp.ih, vp.tile_size, cap);
+    if (int rc = check_ws(B.total, workspace, workspace_bytes)) return rc;
+    char *base = static_cast<char *>(workspace);
+    const Layout L = layout(scene->n, (int64_t)vp.tiles_x * vp.tiles_y, cap, 1);
+    memset(&b, 0, sizeof b);
+    b.nviews = 1;
+    b.vp[0] = vp;
+    b.ws[0] = carve(base, L, cap);
+    b.ws[0].splat_rect = reinterpret_cast<int4 *>(base + B.rect);
+    b.out[0] = ViewOut{image_out ? (void *)image_out : (void *)(base + B.image),
+                       base + B.final_t, reinterpret_cast<int32_t *>(base + B.last), counters,
+                       nullptr, nullptr};
+    return G6R_OK;
+}
+
+int g6r_backward_forward(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
+                         const g6r_config *cfg, void *workspace, size_t workspace_bytes,
+                         int64_t entry_capacity, int64_t *counters, double *image_out,
+                         g6r_stream_t stream) {
+    Batch b;
+    BwdLayout B;
+    if (int rc = bwd_setup(scene, cam, cfg, workspace, workspace_bytes, entry_capacity, counters,
+                           image_out, b, B))
+        return rc;
+    g6r_splat_out so{};
+    so.gids = reinterpret_cast<int64_t *>(static_cast<char *>(workspace) + B.gids);
+    cudaStream_t st = (cudaStream_t)stream;
+    const Layout L = layout(scene->n, (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y, entry_capacity, 1);
+    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
+    if (launch_project(*scene, group_mask, b, &so, true, st)) return cuda_check("project");
+    if (launch_sort(b, st)) return cuda_check("sort");
+    if (launch_ranges(b, st)) return cuda_check("ranges");
+    if (launch_composite(b, true, st)) return cuda_check("composite");
+    return G6R_OK;
+}
+
+int g6r_backward_apply(const g6r_scene *scene, const g6r_camera *cam, const g6r_config *cfg,
+                       void *workspace, size_t workspace_bytes, int64_t entry_capacity,
+                       const double *mu_p, const double *mu_d, const double *cov_raw,
+                       const double *sh, const double *spatial_scale, double directional_scale,
+                       int32_t w_mode, const double *grad_image, double *g_mu_p, double *g_mu_d,
+                       double *g_cov_raw, double *g_sh, double *g_opacity_raw, int64_t *counters,
+                       g6r_stream_t stream) {
+    Batch b;
+    BwdLayout B;
+    if (int rc = bwd_setup(scene, cam, cfg, workspace, workspace_bytes, entry_capacity, counters,
+                           nullptr, b, B))
+        return rc;
+    if (w_mode != 0 && w_mode != 1) return fail(G6R_EINVAL, "w_mode must be 0 or 1");
+    if (!spatial_scale || !grad_image) return fail(G6R_EINVAL, "NULL argument");
+    if (scene->n > 0 && (!mu_p || !mu_d || !cov_raw || !sh || !g_mu_p || !g_mu_d || !g_cov_raw ||
+                         !g_sh || !g_opacity_raw))
+        return fail(G6R_EINVAL, "NULL scene or gradient array");
+    char *base = static_cast<char *>(workspace);
+    const int rc = launch_backward(
+        b.vp[0], *scene, b.ws[0], counters, reinterpret_cast<double *>(base + B.final_t),
+        reinterpret_cast<int32_t *>(base + B.last), grad_image,
+        reinterpret_cast<int64_t *>(base + B.gids), reinterpret_cast<double *>(base + B.egrad),
+        reinterpret_cast<double *>(base + B.gsplat), mu_p, mu_d, cov_raw, sh, spatial_scale,
+        directional_scale, w_mode, g_mu_p, g_mu_d, g_cov_raw, g_sh, g_opacity_raw,
+        (cudaStream_t)stream);
+    if (rc) return rc == G6R_EINVAL ? fail(rc, "backward: bad view") : cuda_check("backward");
+    return G6R_OK;
+}
+
 int g6r_render_backward(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
                         const g6r_config *cfg, void *workspace, size_t workspace_bytes,
                         int64_t entry_capacity, const double *mu_p, const double *mu_d,
@@ -434,47 +512,64 @@ int g6r_render_backward(const g6r_scene *scene, uint32_t group_mask, const g6r_c
                         double *g_mu_p, double *g_mu_d, double *g_cov_raw, double *g_sh,
                         double *g_opacity_raw, int64_t *counters, double *image_out,
                         g6r_stream_t stream) {
-    if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL");
-    if (int rc = check_config(cfg)) return rc;
-    if (cfg->precision != 1) return fail(G6R_EINVAL, "the backward pass runs in f64 (precision=1)");
-    if (cfg->tile_size != 16) return fail(G6R_EINVAL, "the backward kernel supports tile_size 16");
-    if (w_mode != 0 && w_mode != 1) return fail(G6R_EINVAL, "w_mode must be 0 or 1");
-    if (!spatial_scale || !counters || !grad_image) return fail(G6R_EINVAL, "NULL argument");
-    if (scene->n > 0 && (!mu_p || !mu_d || !cov_raw || !sh || !g_mu_p || !g_mu_d || !g_cov_raw ||
-                         !g_sh || !g_opacity_raw))
-        return fail(G6R_EINVAL, "NULL scene or gradient array");
-    if (int rc = check_cap(entry_capacity)) return rc;
-    ViewParams vp;
-    if (int rc = make_view(cam, cfg, vp)) return rc;
-    const BwdLayout B = bwd_layout(scene->n, vp.iw, vp.ih, vp.tile_size, entry_capacity);
-    if (int rc = check_ws(B.total, workspace, workspace_bytes)) return rc;
-    char *base = static_cast<char *>(workspace);
-    const int64_t tiles = (int64_t)vp.tiles_x * vp.tiles_y;
-    const Layout L = layout(scene->n, tiles, entry_capacity, 1);
-    Batch b;
-    memset(&b, 0, sizeof b);
-    b.nviews = 1;
-    b.vp[0] = vp;
-    b.ws[0] = carve(base, L, entry_capacity);
-    b.ws[0].splat_rect = reinterpret_cast<int4 *>(base + B.rect);
-    double *final_t = reinterpret_cast<double *>(base + B.final_t);
-    int32_t *last = reinterpret_cast<int32_t *>(base + B.last);
-    int64_t *gids = reinterpret_cast<int64_t *>(base + B.gids);
-    b.out[0] = ViewOut{image_out ? (void *)image_out : (void *)(base + B.image), final_t, last, counters, nullptr, nullptr};
-    g6r_splat_out so{};
-    so.gids = gids;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
-    if (launch_project(*scene, group_mask, b, &so, true, st)) return cuda_check("project");
-    if (launch_sort(b, st)) return cuda_check("sort");
-    if (launch_ranges(b, st)) return cuda_check("ranges");
-    if (launch_composite(b, true, st)) return cuda_check("composite");
-    const int rc = launch_backward(vp, *scene, b.ws[0], counters, final_t, last, grad_image, gids,
-                                   reinterpret_cast<double *>(base + B.egrad),
-                                   reinterpret_cast<double *>(base + B.gsplat), mu_p, mu_d, cov_raw,
-                                   sh, spatial_scale, directional_scale, w_mode, g_mu_p, g_mu_d,
-                                   g_cov_raw, g_sh, g_opacity_raw, st);
-    if (rc) return rc == G6R_EINVAL ? fail(rc, "backward: bad view") : cuda_check("backward");
+    if (int rc = g6r_backward_forward(scene, group_mask, cam, cfg, workspace, workspace_bytes,
+                                      entry_capacity, counters, image_out, stream))
+        return rc;
+    return g6r_backward_apply(scene, cam, cfg, workspace, workspace_bytes, entry_capacity, mu_p,
+                              mu_d, cov_raw, sh, spatial_scale, directional_scale, w_mode,
+                              grad_image, g_mu_p, g_mu_d, g_cov_raw, g_sh, g_opacity_raw, counters,
+                              stream);
+}
+
+int g6r_decode_records(int64_t n, const void *records, double *mu_p, double *mu_d,
+                       double *cov_raw, double *sh, double *opacity_raw, uint8_t *labels,
+                       int32_t *bad, g6r_stream_t stream) {
+    if (n < 0) return fail(G6R_EINVAL, "decode: n must be >= 0");
+    if (n && (!records || !mu_p || !mu_d || !cov_raw || !sh || !opacity_raw || !labels || !bad))
+        return fail(G6R_EINVAL, "decode: null pointer");
+    if (reinterpret_cast<uintptr_t>(records) & 7) return fail(G6R_EINVAL, "decode: records must be 8-byte aligned");
+    if (launch_decode_records(n, records, mu_p, mu_d, cov_raw, sh, opacity_raw, labels, bad,
+                              (cudaStream_t)stream))
+        return cuda_check("decode_records");
+    return G6R_OK;
+}
+
+size_t g6r_loss_workspace_bytes(int32_t width, int32_t height) {
+    if (width <= 0 || height <= 0) return 0;
+    return loss_workspace_bytes(height, width);
+}
+
+int g6r_loss_grad(const double *pred, const double *target, int32_t target_channels,
+                  int32_t width, int32_t height, double lambda_l1, double lambda_ssim,
+                  int32_t scales, const double *weights, void *workspace, size_t workspace_bytes,
+                  double *grad_out, double *parts, g6r_stream_t stream) {
+    if (!pred || !target || !grad_out || !parts || !workspace)
+        return fail(G6R_EINVAL, "loss: null pointer");
+    if (target_channels != 3 && target_channels != 4)
+        return fail(G6R_EINVAL, "loss: target must have 3 or 4 channels");
+    if (width < 11 || height < 11) return fail(G6R_EINVAL, "loss: images must be >= 11 px per side");
+    if (scales < 1 || scales > 5 || !weights) return fail(G6R_EINVAL, "loss: scales must be 1..5");
+    if (lambda_l1 < 0.0 || lambda_ssim < 0.0 || (lambda_l1 == 0.0 && lambda_ssim == 0.0))
+        return fail(G6R_EINVAL, "loss: weights must be non-negative, one positive");
+    if (workspace_bytes < loss_workspace_bytes(height, width))
+        return fail(G6R_EINVAL, "loss: workspace too small");
+    if (loss_grad(pred, target, target_channels, height, width, lambda_l1, lambda_ssim, scales,
+                  weights, workspace, grad_out, parts, (cudaStream_t)stream))
+        return cuda_check("loss_grad");
+    return G6R_OK;
+}
+
+int g6r_adam_step(int64_t count, double *param, const double *grad, double *m, double *v,
+                  double lr, double bias1, double bias2, g6r_stream_t stream) {
+    if (count < 0) return fail(G6R_EINVAL, "adam: count must be >= 0");
+    if (adam_step(count, param, grad, m, v, lr, bias1, bias2, (cudaStream_t)stream))
+        return cuda_check("adam_step");
+    return G6R_OK;
+}
+
+int g6r_any_nonfinite(int64_t count, const double *x, int32_t *flag, g6r_stream_t stream) {
+    if (count < 0) return fail(G6R_EINVAL, "nonfinite: count must be >= 0");
+    if (nonfinite(count, x, flag, (cudaStream_t)stream)) return cuda_check("nonfinite");
     return G6R_OK;
 }
 

@@ -60,6 +60,9 @@ int launch_prepare(int64_t n, const double *mu_p, const double *mu_d, const doub
                    const double *sh, const double *opacity_raw, const uint8_t *labels,
                    const double *ss, double ds, int w_mode, double *records, uint8_t *flags,
                    int64_t *label_counts, cudaStream_t st);
+int launch_decode_records(int64_t n, const void *recs, double *mu_p, double *mu_d, double *cov_raw,
+                          double *sh, double *opacity_raw, uint8_t *labels, int32_t *bad,
+                          cudaStream_t st);
 int launch_pack_records(int64_t n, const double *mu_p, const double *mu_d, const double *sh,
                         const double *opacity, const double *w_norm, const double *adjust,
                         const double *prec, const double *sigma_prime, const uint8_t *degenerate,
@@ -114,5 +117,14 @@ int sort_passes(int tiles);   // upper bound on radix passes for `tiles` tiles
 // g6r_trace_dump prints per-launch device intervals.  Off by default (one
 // branch per launch).
 void trace_mark(const char *label, cudaStream_t st);
+
+// fine-tune loop (g6r_train.cu)
+size_t loss_workspace_bytes(int h, int w);
+int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
+              double lambda_ssim, int scales, const double *weights, void *ws, double *grad,
+              double *parts, cudaStream_t st);
+int adam_step(int64_t n, double *p, const double *g, double *m, double *v, double lr, double bias1,
+              double bias2, cudaStream_t st);
+int nonfinite(int64_t n, const double *x, int32_t *flag, cudaStream_t st);
 
 }  // namespace g6r

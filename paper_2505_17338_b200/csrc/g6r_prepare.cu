@@ -197,4 +197,57 @@ int launch_pack_records(int64_t n, const double *mu_p, const double *mu_d, const
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
+// --- scene ingest: G6DS record block -> f64 SoA (sceneio.py:77-111) ---------
+// One CTA stages 128 contiguous 168-byte records (21 KiB) through shared
+// memory with coalesced 8-byte loads, then writes every output field with
+// consecutive threads on consecutive output doubles.  HBM-bound: 168 B read
+// and 320 B + 1 B written per Gaussian.
+constexpr int kDecodeRecs = 128;
+constexpr int kRecWords = 21;   // 168 bytes as u64
+
+__global__ void __launch_bounds__(kBlock)
+k_decode_records(int64_t n, const unsigned long long *__restrict__ recs, double *__restrict__ mu_p,
+                 double *__restrict__ mu_d, double *__restrict__ cov_raw, double *__restrict__ sh,
+                 double *__restrict__ opacity_raw, uint8_t *__restrict__ labels,
+                 int32_t *__restrict__ bad) {
+    __shared__ unsigned long long s[kDecodeRecs * kRecWords];
+    const int64_t first = (int64_t)blockIdx.x * kDecodeRecs;
+    const int cnt = (int)(n - first < kDecodeRecs ? n - first : kDecodeRecs);
+    const unsigned long long *src = recs + first * kRecWords;
+    for (int k = threadIdx.x; k < cnt * kRecWords; k += blockDim.x) s[k] = src[k];
+    __syncthreads();
+    const float *f = reinterpret_cast<const float *>(s);              // 42 floats per record
+    const uint8_t *b = reinterpret_cast<const uint8_t *>(s);          // 168 bytes per record
+    bool oops = false;
+    struct Field { double *out; int off, width; };
+    const Field fields[5] = {{mu_p, 0, 3}, {mu_d, 3, 3}, {cov_raw, 6, 21}, {sh, 27, 12},
+                             {opacity_raw, 39, 1}};
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const Field fd = fields[q];
+        for (int k = threadIdx.x; k < cnt * fd.width; k += blockDim.x) {
+            const int r = k / fd.width, c = k - r * fd.width;
+            const float v = f[r * 42 + fd.off + c];
+            oops |= !isfinite(v);
+            fd.out[first * fd.width + k] = (double)v;
+        }
+    }
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+        const uint8_t l = b[r * 168 + 160];
+        oops |= l < 1 || l > 11;
+        labels[first + r] = l;
+    }
+    if (__syncthreads_or(oops) && threadIdx.x == 0) *bad = 1;
+}
+
+int launch_decode_records(int64_t n, const void *recs, double *mu_p, double *mu_d, double *cov_raw,
+                          double *sh, double *opacity_raw, uint8_t *labels, int32_t *bad,
+                          cudaStream_t st) {
+    if (n == 0) return 0;
+    k_decode_records<<<(unsigned)ceil_div(n, kDecodeRecs), kBlock, 0, st>>>(
+        n, static_cast<const unsigned long long *>(recs), mu_p, mu_d, cov_raw, sh, opacity_raw,
+        labels, bad);
+    return cudaGetLastError() != cudaSuccess;
+}
+
 }  // namespace g6r

@@ -1,0 +1,402 @@
+// g6r_train.cu -- photometric loss with its image gradient, and Adam, on device
+// (the fine-tune loop of diffrender.py:548-585 around the render path).
+//
+// Replaces diffrender.py:117-138 (_loss_parts: L1 + (1 - MS-SSIM)),
+// _ssim.py:23-201 (11x11 sigma-1.5 valid windows, 2x2 pooling pyramid,
+// per-scale contrast-structure means, analytic gradient) and
+// diffrender.py:481-509 (adam_step).  Reductions are deterministic (fixed
+// block partials, then one ordered final sum); Adam follows the reference's
+// operation order element for element.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "g6r_common.cuh"
+#include "g6r_internal.h"
+
+namespace g6r {
+
+constexpr int kWin = 11;
+constexpr int kRedBlocks = 256;   // fixed partial count for deterministic sums
+__constant__ double c_win[kWin];
+
+// Gaussian window (_ssim.py:25-30): exp(-x^2 / (2 s^2)) normalised, s = 1.5.
+static void window_host(double *w) {
+    double s = 0.0;
+    for (int k = 0; k < kWin; ++k) {
+        const double x = k - (kWin - 1) / 2.0;
+        w[k] = std::exp(-(x * x) / (2.0 * 1.5 * 1.5));
+        s += w[k];
+    }
+    for (int k = 0; k < kWin; ++k) w[k] /= s;
+}
+
+// planar channel c of an interleaved (H, W, C) image
+__global__ void k_extract(const double *__restrict__ img, int C, int c, int64_t hw,
+                          double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = img[i * C + c];
+}
+
+// 5 statistic planes x, y, x*x, y*y, x*y
+__global__ void k_products(const double *__restrict__ x, const double *__restrict__ y, int64_t hw,
+                           double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = x[i], b = y[i];
+        out[i] = a;
+        out[hw + i] = b;
+        out[2 * hw + i] = a * a;
+        out[3 * hw + i] = b * b;
+        out[4 * hw + i] = a * b;
+    }
+}
+
+// 1-D correlation with the window along one axis of `planes` (h, w) planes.
+// valid: out length n - 10; full: n + 10 (zero padding, the adjoint).
+__global__ void k_corr1d(const double *__restrict__ in, double *__restrict__ out, int planes, int h,
+                         int w, int axis, int full) {
+    const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
+    const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
+    const int64_t per = (int64_t)oh * ow;
+    const int shift = full ? kWin - 1 : 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < per * planes;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(q / per);
+        const int64_t r = q % per;
+        const int i = (int)(r / ow), j = (int)(r % ow);
+        const double *src = in + (int64_t)p * h * w;
+        double s = 0.0;
+        for (int k = 0; k < kWin; ++k) {
+            const int ii = axis == 0 ? i + k - shift : i;
+            const int jj = axis == 1 ? j + k - shift : j;
+            if (ii >= 0 && ii < h && jj >= 0 && jj < w) s += c_win[k] * src[(int64_t)ii * w + jj];
+        }
+        out[q] = s;
+    }
+}
+
+// SSIM window maps (_ssim.py:66-84) from the 5 correlated statistics
+__global__ void k_ssim_maps(const double *__restrict__ st, int64_t n, double *__restrict__ maps) {
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double ux = st[i], uy = st[n + i], exx = st[2 * n + i], eyy = st[3 * n + i], exy = st[4 * n + i];
+        const double sxx = exx - ux * ux, syy = eyy - uy * uy, sxy = exy - ux * uy;
+        const double b1 = ux * ux + uy * uy + C1;
+        const double b2 = sxx + syy + C2;
+        maps[i] = ux;
+        maps[n + i] = uy;
+        maps[2 * n + i] = b1;
+        maps[3 * n + i] = b2;
+        maps[4 * n + i] = (2.0 * ux * uy + C1) / b1;   // l
+        maps[5 * n + i] = (2.0 * sxy + C2) / b2;       // cs
+    }
+}
+
+// deterministic partial sums: block b sums a fixed strided subset
+__global__ void k_partials(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                           double *__restrict__ part) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += b ? a[i] * b[i] : a[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void k_sum_partials(const double *__restrict__ part, int n, double *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += part[i];
+        *out = s;
+    }
+}
+
+// per-window gradients of SsimParts.backward (_ssim.py:86-98) for constant
+// per-window upstream gradients g_lcs, g_cs
+__global__ void k_ssim_bwd_maps(const double *__restrict__ maps, int64_t n, double g_lcs, double g_cs,
+                                double *__restrict__ gm) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double ux = maps[i], uy = maps[n + i], b1 = maps[2 * n + i], b2 = maps[3 * n + i];
+        const double l = maps[4 * n + i], cs = maps[5 * n + i];
+        const double g_l = g_lcs * cs;
+        const double g_cst = g_lcs * l + g_cs;
+        gm[i] = g_l * 2.0 * (uy - l * ux) / b1 + g_cst * 2.0 * (cs * ux - uy) / b2;   // g_ux
+        gm[n + i] = -g_cst * cs / b2;                                                  // g_exx
+        gm[2 * n + i] = g_cst * 2.0 / b2;                                              // g_exy
+    }
+}
+
+// g += adj(g_ux) + 2 x adj(g_exx) + y adj(g_exy)
+__global__ void k_ssim_bwd_combine(const double *__restrict__ adj, const double *__restrict__ x,
+                                   const double *__restrict__ y, int64_t hw, double *__restrict__ g) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
+        g[i] += adj[i] + 2.0 * x[i] * adj[hw + i] + y[i] * adj[2 * hw + i];
+}
+
+// 2x2 average pooling (_ssim.py:47-51) and its adjoint (:54-62)
+__global__ void k_pool2(const double *__restrict__ in, int h, int w, double *__restrict__ out) {
+    const int h2 = h / 2, w2 = w / 2;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)h2 * w2;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(q / w2), j = (int)(q % w2);
+        const double *r0 = in + (int64_t)(2 * i) * w + 2 * j, *r1 = r0 + w;
+        out[q] = 0.25 * (r0[0] + r1[0] + r0[1] + r1[1]);
+    }
+}
+
+__global__ void k_pool2_adjoint(const double *__restrict__ g2, int h, int w, double *__restrict__ out) {
+    const int h2 = h / 2, w2 = w / 2;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)h * w;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(q / w), j = (int)(q % w);
+        out[q] = (i < 2 * h2 && j < 2 * w2) ? 0.25 * g2[(int64_t)(i / 2) * w2 + j / 2] : 0.0;
+    }
+}
+
+// L1 part: diff statistics and grad = l1_w * sign(diff) / size on RGB
+__global__ void k_l1(const double *__restrict__ pred, const double *__restrict__ tgt, int tc,
+                     int64_t hw, double scale, double *__restrict__ grad, double *__restrict__ absdiff) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hw * 3; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = q / 3;
+        const int c = (int)(q % 3);
+        const double d = pred[p * 4 + c] - tgt[p * tc + c];
+        absdiff[q] = fabs(d);
+        grad[p * 4 + c] = scale * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0));
+        if (c == 0) grad[p * 4 + 3] = 0.0;
+    }
+}
+
+__global__ void k_axpy_channel(const double *__restrict__ g, int64_t hw, int c, double alpha,
+                               double *__restrict__ grad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
+        grad[i * 4 + c] += alpha * g[i];
+}
+
+// bias-corrected Adam (diffrender.py:493-508), the reference's operation order
+__global__ void k_adam(int64_t n, double *__restrict__ p, const double *__restrict__ g,
+                       double *__restrict__ m, double *__restrict__ v, double lr, double bias1,
+                       double bias2) {
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double gi = g[i];
+        double mi = m[i] * b1;
+        mi = mi + (1.0 - b1) * gi;
+        double vi = v[i] * b2;
+        vi = vi + (1.0 - b2) * (gi * gi);
+        m[i] = mi;
+        v[i] = vi;
+        p[i] = p[i] - lr * (mi / bias1) / (sqrt(vi / bias2) + eps);
+    }
+}
+
+__global__ void k_nonfinite(int64_t n, const double *__restrict__ x, int32_t *__restrict__ flag) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+static unsigned grid_for(int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8));
+}
+
+// --- host orchestration -------------------------------------------------------
+
+struct LossLayout {
+    size_t x[5], y[5], maps[5], stats, tmp, gm, adj, g, part, scal, absd, total;
+};
+
+static inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+static LossLayout loss_layout(int h, int w, int scales) {
+    LossLayout L{};
+    size_t o = 0;
+    int hh = h, ww = w;
+    for (int j = 0; j < scales; ++j) {
+        const size_t hw = (size_t)hh * ww;
+        const size_t nv = (size_t)std::max(hh - kWin + 1, 0) * std::max(ww - kWin + 1, 0);
+        L.x[j] = o;
+        o = al(o + hw * 8);
+        L.y[j] = o;
+        o = al(o + hw * 8);
+        L.maps[j] = o;
+        o = al(o + 6 * nv * 8);
+        hh /= 2;
+        ww /= 2;
+    }
+    const size_t hw = (size_t)h * w;
+    L.stats = o;
+    o = al(o + 5 * hw * 8);
+    L.tmp = o;
+    o = al(o + 5 * hw * 8);
+    L.gm = o;
+    o = al(o + 3 * hw * 8);
+    L.adj = o;
+    o = al(o + 3 * hw * 8);
+    L.g = o;
+    o = al(o + 2 * hw * 8);
+    L.part = o;
+    o = al(o + kRedBlocks * 8);
+    L.scal = o;
+    o = al(o + 64 * 8);
+    L.absd = o;
+    o = al(o + 3 * hw * 8);
+    L.total = o;
+    return L;
+}
+
+size_t loss_workspace_bytes(int h, int w) { return loss_layout(h, w, 5).total; }
+
+// sum of a*b (or a) over n doubles, deterministic; result read back to host
+static double dsum(const double *a, const double *b, int64_t n, double *part, double *scal,
+                   cudaStream_t st) {
+    k_partials<<<kRedBlocks, 256, 0, st>>>(a, b, n, part);
+    k_sum_partials<<<1, 32, 0, st>>>(part, kRedBlocks, scal);
+    double out = 0.0;
+    cudaMemcpyAsync(&out, scal, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return out;
+}
+
+int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
+              double lambda_ssim, int scales, const double *weights_in, void *ws, double *grad,
+              double *parts, cudaStream_t st) {
+    static bool win_set[64] = {};   // __constant__ lives per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return G6R_EINVAL;
+    if (!win_set[dev]) {
+        double wv[kWin];
+        window_host(wv);
+        cudaMemcpyToSymbol(c_win, wv, sizeof wv);
+        win_set[dev] = true;
+    }
+    char *base = static_cast<char *>(ws);
+    const int64_t hw = (int64_t)h * w;
+    const LossLayout L = loss_layout(h, w, 5);
+    double *part = reinterpret_cast<double *>(base + L.part);
+    double *scal = reinterpret_cast<double *>(base + L.scal);
+    // L1 (diffrender.py:126-129)
+    double *absd = reinterpret_cast<double *>(base + L.absd);
+    k_l1<<<grid_for(hw * 3), 256, 0, st>>>(pred, tgt, tc, hw, lambda_l1 / (double)(hw * 3), grad, absd);
+    const double l1 = dsum(absd, nullptr, hw * 3, part, scal, st) / (double)(hw * 3);
+    double ssim_value = 0.0;
+    if (lambda_ssim > 0.0) {
+        // effective_scales (_ssim.py:116-120)
+        const int ns = std::min(h, w) < (1 << (scales - 1)) * kWin ? 1 : scales;
+        std::vector<double> wts(ns);
+        double wsum = 0.0;
+        for (int j = 0; j < ns; ++j) wsum += weights_in[j];
+        for (int j = 0; j < ns; ++j) wts[j] = weights_in[j] / wsum;
+        double total = 0.0;
+        for (int c = 0; c < 3; ++c) {
+            int hs[5], wsz[5];
+            double *xs[5], *ys[5], *mp[5];
+            hs[0] = h;
+            wsz[0] = w;
+            for (int j = 0; j < ns; ++j) {
+                xs[j] = reinterpret_cast<double *>(base + L.x[j]);
+                ys[j] = reinterpret_cast<double *>(base + L.y[j]);
+                mp[j] = reinterpret_cast<double *>(base + L.maps[j]);
+                if (j > 0) {
+                    hs[j] = hs[j - 1] / 2;
+                    wsz[j] = wsz[j - 1] / 2;
+                }
+            }
+            k_extract<<<grid_for(hw), 256, 0, st>>>(pred, 4, c, hw, xs[0]);
+            k_extract<<<grid_for(hw), 256, 0, st>>>(tgt, tc, c, hw, ys[0]);
+            double terms[5], counts[5];
+            for (int j = 0; j < ns; ++j) {
+                const int hj = hs[j], wj = wsz[j];
+                const int64_t hwj = (int64_t)hj * wj;
+                const int hv = hj - kWin + 1, wv = wj - kWin + 1;
+                const int64_t nv = (int64_t)hv * wv;
+                double *stats = reinterpret_cast<double *>(base + L.stats);
+                double *tmp = reinterpret_cast<double *>(base + L.tmp);
+                k_products<<<grid_for(hwj), 256, 0, st>>>(xs[j], ys[j], hwj, stats);
+                k_corr1d<<<grid_for(5 * (int64_t)hv * wj), 256, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0);
+                k_corr1d<<<grid_for(5 * nv), 256, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0);
+                k_ssim_maps<<<grid_for(nv), 256, 0, st>>>(stats, nv, mp[j]);
+                const bool last = j == ns - 1;
+                const double s = last ? dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, part, scal, st)
+                                      : dsum(mp[j] + 5 * nv, nullptr, nv, part, scal, st);
+                terms[j] = s / (double)nv;
+                counts[j] = (double)nv;
+                if (j + 1 < ns) {
+                    k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(xs[j], hj, wj, xs[j + 1]);
+                    k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(ys[j], hj, wj, ys[j + 1]);
+                }
+            }
+            double value;
+            if (ns == 1) {
+                value = terms[0];
+            } else {
+                value = 1.0;
+                for (int j = 0; j < ns; ++j) value *= std::pow(std::max(terms[j], 0.0), wts[j]);
+            }
+            // backward from the coarsest scale (_ssim.py:175-198)
+            double *g = reinterpret_cast<double *>(base + L.g);
+            double *g2 = g + hw;
+            cudaMemsetAsync(g, 0, (size_t)hs[ns - 1] * wsz[ns - 1] * 8, st);
+            for (int j = ns - 1; j >= 0; --j) {
+                const int hj = hs[j], wj = wsz[j];
+                const int64_t hwj = (int64_t)hj * wj;
+                const int hv = hj - kWin + 1, wv = wj - kWin + 1;
+                const int64_t nv = (int64_t)hv * wv;
+                if (j < ns - 1) {   // upsample the coarser gradient into this level
+                    k_pool2_adjoint<<<grid_for(hwj), 256, 0, st>>>(g, hj, wj, g2);
+                    std::swap(g, g2);
+                }
+                double g_lcs = 0.0, g_cs = 0.0;
+                bool go = false;
+                if (ns == 1) {
+                    g_lcs = 1.0 / counts[0];
+                    go = true;
+                } else if (value > 0.0 && terms[j] > 0.0) {
+                    const double per = value * wts[j] / terms[j] / counts[j];
+                    if (j == ns - 1) g_lcs = per;
+                    else g_cs = per;
+                    go = true;
+                }
+                if (go) {
+                    double *gm = reinterpret_cast<double *>(base + L.gm);
+                    double *tmp = reinterpret_cast<double *>(base + L.tmp);
+                    double *adj = reinterpret_cast<double *>(base + L.adj);
+                    k_ssim_bwd_maps<<<grid_for(nv), 256, 0, st>>>(mp[j], nv, g_lcs, g_cs, gm);
+                    k_corr1d<<<grid_for(3 * (int64_t)hj * wv), 256, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
+                    k_corr1d<<<grid_for(3 * hwj), 256, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
+                    k_ssim_bwd_combine<<<grid_for(hwj), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g);
+                }
+            }
+            // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
+            k_axpy_channel<<<grid_for(hw), 256, 0, st>>>(g, hw, c, -lambda_ssim / 3.0, grad);
+            total += value;
+        }
+        ssim_value = total / 3.0;
+    }
+    const double ssim_loss = lambda_ssim > 0.0 ? 1.0 - ssim_value : 0.0;
+    parts[0] = lambda_l1 * l1 + lambda_ssim * ssim_loss;
+    parts[1] = l1;
+    parts[2] = ssim_loss;
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int adam_step(int64_t n, double *p, const double *g, double *m, double *v, double lr, double bias1,
+              double bias2, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    k_adam<<<grid_for(n), 256, 0, st>>>(n, p, g, m, v, lr, bias1, bias2);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+int nonfinite(int64_t n, const double *x, int32_t *flag, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    k_nonfinite<<<grid_for(n), 256, 0, st>>>(n, x, flag);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+}  // namespace g6r

@@ -119,3 +119,451 @@ def render_backward(scene, camera, grad_image, group_mask=None,
     if not g.any():
         return GradientBuffer.zeros(len(scene.mu_p))
     return render_backward_device(scene, camera, g, group_mask, config).to_host()
+
+
+# ---------------------------------------------------------------------------
+# Fine-tune loop on the device (diffrender.py:55-138, 442-585 of the reference)
+# ---------------------------------------------------------------------------
+
+ADAM_BETA1 = 0.9
+ADAM_BETA2 = 0.999
+ADAM_EPS = 1e-8
+POLY_POWER = 0.9
+DEFAULT_LR_SCALE = {"mu_p": 0.1}
+TRACE_FIELDS = ("iteration", "lr", "l1", "ssim_loss", "total")
+DEFAULT_WEIGHTS = (0.0448, 0.2856, 0.3001, 0.2363, 0.1333)
+_SHAPES = {"mu_p": (3,), "mu_d": (3,), "cov_raw": (21,), "sh": (12,), "opacity_raw": ()}
+
+
+@dataclass(frozen=True)
+class LossConfig:
+    """lambda_l1 * L1 + lambda_ssim * (1 - MS-SSIM); weights normalised at
+    construction (diffrender.py:68-97)."""
+
+    lambda_l1: float = 0.8
+    lambda_ssim: float = 0.2
+    ms_ssim_scales: int = 5
+    ms_ssim_weights: tuple = DEFAULT_WEIGHTS
+
+    def __post_init__(self):
+        if self.lambda_l1 < 0.0 or self.lambda_ssim < 0.0:
+            raise InvalidParameterError("loss weights must be non-negative")
+        if self.lambda_l1 == 0.0 and self.lambda_ssim == 0.0:
+            raise InvalidParameterError("at least one loss weight must be positive")
+        if self.ms_ssim_scales < 1:
+            raise InvalidParameterError("ms_ssim_scales must be >= 1")
+        if self.ms_ssim_scales > 5:
+            raise InvalidParameterError("ms_ssim_scales above 5 are not supported on the device")
+        weights = tuple(float(w) for w in self.ms_ssim_weights)
+        if len(weights) != self.ms_ssim_scales:
+            raise InvalidParameterError(
+                f"need {self.ms_ssim_scales} ms_ssim_weights, got {len(weights)}")
+        if any(w <= 0.0 for w in weights):
+            raise InvalidParameterError("ms_ssim_weights must be positive")
+        total = sum(weights)
+        object.__setattr__(self, "ms_ssim_weights", tuple(w / total for w in weights))
+
+
+class _LossWorkspace:
+    """Per-(device, size) scratch for g6r_loss_grad, reused across calls."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, dev, w, h):
+        import torch
+        key = (dev.index, w, h)
+        ws = cls._cache.get(key)
+        if ws is None:
+            nbytes = nat.load().g6r_loss_workspace_bytes(w, h)
+            ws = cls._cache[key] = (torch.empty(nbytes, dtype=torch.uint8, device=dev), nbytes)
+        return ws
+
+
+def loss_device(pred, target, cfg: LossConfig = None, grad_out=None):
+    """(total, l1, ssim_loss), grad for device tensors: pred (H,W,4) f64,
+    target (H,W,3|4) f64.  One g6r_loss_grad call (synchronises the stream to
+    read the three scalars)."""
+    import torch
+    cfg = cfg or LossConfig()
+    if pred.ndim != 3 or target.ndim != 3 or tuple(pred.shape[:2]) != tuple(target.shape[:2]):
+        raise InvalidParameterError(
+            f"image shapes do not match: {tuple(pred.shape)} vs {tuple(target.shape)}")
+    h, w = int(pred.shape[0]), int(pred.shape[1])
+    if pred.shape[2] != 4 or target.shape[2] not in (3, 4):
+        raise InvalidParameterError("pred must be (H,W,4) and target (H,W,3|4)")
+    ws, nbytes = _LossWorkspace.get(pred.device, w, h)
+    grad = grad_out if grad_out is not None else torch.empty_like(pred)
+    weights = (ctypes.c_double * cfg.ms_ssim_scales)(*cfg.ms_ssim_weights)
+    parts = (ctypes.c_double * 3)()
+    nat.check(nat.load().g6r_loss_grad(
+        _ptr(pred), _ptr(target), int(target.shape[2]), w, h, cfg.lambda_l1, cfg.lambda_ssim,
+        cfg.ms_ssim_scales, ctypes.cast(weights, ctypes.c_void_p), _ptr(ws), nbytes, _ptr(grad),
+        ctypes.cast(parts, ctypes.c_void_p), _stream_handle()))
+    return (parts[0], parts[1], parts[2]), grad
+
+
+def _to_device_image(img, dev, rgb4=False):
+    import torch
+    t = img if isinstance(img, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(img, np.float64))
+    t = t.to(device=dev, dtype=torch.float64).contiguous()
+    if t.ndim != 3:
+        raise InvalidParameterError(f"expected an (H, W, C) image, got shape {tuple(t.shape)}")
+    if rgb4 and t.shape[2] == 3:
+        t = torch.cat([t, torch.zeros_like(t[:, :, :1])], dim=2).contiguous()
+    return t
+
+
+def _loss_parts(pred, gt, cfg: LossConfig):
+    """(total, l1, ssim_loss, d total/d pred) comparing RGB (diffrender.py:117-138)."""
+    import torch
+    from .raster import _require_cuda
+    _require_cuda()
+    pred_a, gt_a = np.asarray(pred, np.float64), np.asarray(gt, np.float64)
+    if pred_a.shape[:2] != gt_a.shape[:2] or pred_a.ndim != 3 or gt_a.ndim != 3:
+        raise InvalidParameterError(f"image shapes do not match: {pred_a.shape} vs {gt_a.shape}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p = _to_device_image(pred_a, dev, rgb4=True)
+    g = _to_device_image(gt_a, dev)
+    if g.shape[2] not in (3, 4):
+        g = g[:, :, :3].contiguous()
+    (total, l1, ssim_loss), grad = loss_device(p, g, cfg)
+    return total, l1, ssim_loss, grad[:, :, :pred_a.shape[2]].cpu().numpy()
+
+
+def loss(pred, gt, cfg: LossConfig = None):
+    """Photometric loss and its analytic gradient with respect to ``pred``
+    (diffrender.py:141-156): (total, grad) with grad shaped like ``pred``."""
+    total, _, _, grad = _loss_parts(pred, gt, cfg or LossConfig())
+    return total, grad
+
+
+def ms_ssim(a, b, scales: int = 5, weights=DEFAULT_WEIGHTS) -> float:
+    """Multi-scale SSIM in [-1, 1] (diffrender.py:100-114); alpha ignored.
+    Single-channel images are evaluated as three identical channels."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.ndim == 2:
+        a = a[:, :, None]
+    if b.ndim == 2:
+        b = b[:, :, None]
+    if a.shape[2] == 4:
+        a = a[:, :, :3]
+    if b.shape[2] == 4:
+        b = b[:, :, :3]
+    if a.shape != b.shape:
+        raise ValueError(f"image shapes differ: {a.shape} vs {b.shape}")
+    if min(a.shape[0], a.shape[1]) < 11:
+        raise ValueError(f"images must be at least 11 px per side, got {a.shape}")
+    if a.shape[2] == 1:
+        a, b = np.repeat(a, 3, axis=2), np.repeat(b, 3, axis=2)
+    elif a.shape[2] != 3:
+        raise ValueError(f"expected 1, 3 or 4 channels, got {a.shape[2]}")
+    cfg = LossConfig(lambda_l1=0.0, lambda_ssim=1.0, ms_ssim_scales=scales,
+                     ms_ssim_weights=tuple(weights[:scales]))
+    _, _, ssim_loss, _ = _loss_parts(np.concatenate([a, np.zeros(a.shape[:2] + (1,))], axis=2), b, cfg)
+    return 1.0 - ssim_loss
+
+
+def polylr(step: int, total: int, base_lr: float) -> float:
+    """``base_lr * (1 - step/total) ** 0.9`` (diffrender.py:442-449)."""
+    if total <= 0:
+        raise InvalidParameterError(f"total must be positive, got {total}")
+    if not 0 <= step <= total:
+        raise InvalidParameterError(f"step {step} outside [0, {total}]")
+    return base_lr * (1.0 - step / total) ** POLY_POWER
+
+
+@dataclass
+class OptimizerState:
+    """Adam moments per parameter group plus the lr schedule (diffrender.py:452-465)."""
+
+    m: dict
+    v: dict
+    step: int
+    total_steps: int
+    base_lr: float
+    lr_scale: dict = None
+    skipped: int = 0
+
+    def __post_init__(self):
+        if self.lr_scale is None:
+            self.lr_scale = dict(DEFAULT_LR_SCALE)
+
+    def lr(self) -> float:
+        return polylr(self.step, self.total_steps, self.base_lr)
+
+
+def init_optimizer(scene, total_steps: int, base_lr: float = 1e-3,
+                   lr_scale: dict = None) -> OptimizerState:
+    """Zero-moment Adam state sized for ``scene`` (diffrender.py:468-478)."""
+    if total_steps <= 0:
+        raise InvalidParameterError(f"total_steps must be positive, got {total_steps}")
+    shapes = {name: np.shape(getattr(scene, name)) for name in PARAM_GROUPS}
+    return OptimizerState(m={k: np.zeros(s) for k, s in shapes.items()},
+                          v={k: np.zeros(s) for k, s in shapes.items()},
+                          step=0, total_steps=total_steps, base_lr=base_lr,
+                          lr_scale=dict(DEFAULT_LR_SCALE if lr_scale is None else lr_scale))
+
+
+def _with_params(scene, **arrays):
+    if hasattr(scene, "with_params"):
+        return scene.with_params(**arrays)
+    return replace(scene, **arrays)
+
+
+def adam_step(state: OptimizerState, grads: GradientBuffer, scene):
+    """One bias-corrected Adam update (diffrender.py:481-509) through
+    g6r_adam_step; a non-finite gradient anywhere skips the update."""
+    import torch
+    from .raster import _require_cuda
+    _require_cuda()
+    if not grads.all_finite():
+        state.skipped += 1
+        return scene, state
+    lr_now = polylr(state.step, state.total_steps, state.base_lr)
+    state.step += 1
+    t = state.step
+    bias1 = 1.0 - ADAM_BETA1 ** t
+    bias2 = 1.0 - ADAM_BETA2 ** t
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = nat.load()
+    updates = {}
+    for name, g in grads.groups():
+        up = [torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev)
+              for a in (getattr(scene, name), g, state.m[name], state.v[name])]
+        lr_g = lr_now * state.lr_scale.get(name, 1.0)
+        nat.check(lib.g6r_adam_step(up[0].numel(), *[_ptr(a) for a in up], lr_g, bias1, bias2,
+                                    _stream_handle()))
+        updates[name] = up[0].cpu().numpy()
+        state.m[name] = up[2].cpu().numpy()
+        state.v[name] = up[3].cpu().numpy()
+    return _with_params(scene, **updates), state
+
+
+def write_trace(history, path) -> None:
+    """Fine-tune trace rows as CSV (diffrender.py:512-517)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        writer = csv.DictWriter(fh, fieldnames=TRACE_FIELDS)
+        writer.writeheader()
+        writer.writerows(history)
+
+
+def save_checkpoint(scene, state: OptimizerState, path) -> None:
+    """G6DS scene at ``path`` plus an optimizer sidecar ``path + '.opt.npz'``
+    (diffrender.py:520-531)."""
+    from .sceneio import save_scene
+    save_scene(scene, path)
+    arrays = {f"m_{k}": state.m[k] for k in PARAM_GROUPS}
+    arrays.update({f"v_{k}": state.v[k] for k in PARAM_GROUPS})
+    names = sorted(state.lr_scale)
+    np.savez(str(path) + ".opt.npz", step=state.step, total_steps=state.total_steps,
+             base_lr=state.base_lr, skipped=state.skipped,
+             lr_scale_names=np.array(names, dtype=object),
+             lr_scale_values=np.array([state.lr_scale[k] for k in names]), **arrays)
+
+
+def load_checkpoint(path):
+    """Inverse of :func:`save_checkpoint` (diffrender.py:534-545)."""
+    from .sceneio import load_scene
+    scene = load_scene(path)
+    with np.load(str(path) + ".opt.npz", allow_pickle=True) as z:
+        state = OptimizerState(
+            m={k: z[f"m_{k}"] for k in PARAM_GROUPS}, v={k: z[f"v_{k}"] for k in PARAM_GROUPS},
+            step=int(z["step"]), total_steps=int(z["total_steps"]), base_lr=float(z["base_lr"]),
+            skipped=int(z["skipped"]),
+            lr_scale=dict(zip(z["lr_scale_names"].tolist(), z["lr_scale_values"].tolist())))
+    return scene, state
+
+
+class DeviceTrainer:
+    """The fine-tune state resident on one GPU: the 40 raw parameters, Adam
+    moments, gradients, view targets and all scratch, as device tensors.
+
+    ``step(view)`` runs one iteration of the reference loop
+    (diffrender.py:570-581) as native calls on the current stream:
+    g6r_prepare -> g6r_backward_forward (f64 render, state kept) ->
+    g6r_loss_grad -> g6r_backward_apply -> g6r_any_nonfinite ->
+    g6r_adam_step x5.  Host synchronisation: the degenerate-policy counts,
+    the overflow counter, the loss scalars and the non-finite flag."""
+
+    def __init__(self, scene, views, loss_cfg: LossConfig = None, config: RenderConfig = None,
+                 total_steps: int = 1, base_lr: float = 1e-3, lr_scale: dict = None):
+        import torch
+        from .raster import _require_cuda
+        _require_cuda()
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.loss_cfg = loss_cfg or LossConfig()
+        self.cfg = replace(config if config is not None else DEFAULT_CONFIG, precision="f64")
+        if int(self.cfg.tile_size) != 16:
+            raise InvalidParameterError("the backward pass supports tile_size 16")
+        self.ccfg = _check_config(self.cfg)
+        self.scene = scene
+        self.n = n = len(scene.mu_p)
+
+        def up(a):
+            if isinstance(a, torch.Tensor):
+                return a.to(device=self.dev, dtype=torch.float64).clone().contiguous()
+            return torch.from_numpy(np.array(a, dtype=np.float64)).to(self.dev)
+
+        self.params = {k: up(getattr(scene, k)) for k in PARAM_GROUPS}
+        lab = scene.labels
+        self.labels = (lab.to(self.dev, torch.uint8).contiguous() if isinstance(lab, torch.Tensor)
+                       else torch.from_numpy(np.ascontiguousarray(lab, np.uint8)).to(self.dev))
+        self.m = {k: torch.zeros_like(t) for k, t in self.params.items()}
+        self.v = {k: torch.zeros_like(t) for k, t in self.params.items()}
+        self.grads = {k: torch.empty((max(n, 1),) + _SHAPES[k], dtype=torch.float64,
+                                     device=self.dev) for k in PARAM_GROUPS}
+        self.step_count, self.total_steps, self.base_lr, self.skipped = 0, total_steps, base_lr, 0
+        self.lr_scale = dict(DEFAULT_LR_SCALE if lr_scale is None else lr_scale)
+        self.views = []
+        for cam, target in views:
+            t = _to_device_image(target, self.dev)
+            if tuple(t.shape[:2]) != (int(cam.height), int(cam.width)) or t.shape[2] not in (3, 4):
+                raise InvalidParameterError(
+                    f"target shape {tuple(t.shape)} does not match the camera "
+                    f"({int(cam.height)}, {int(cam.width)}, 3|4)")
+            self.views.append((cam, t))
+        ss = np.broadcast_to(np.asarray(scene.spatial_scale, np.float64), (3,))
+        self.ss = (ctypes.c_double * 3)(*ss.tolist())
+        self.directional_scale = float(scene.directional_scale)
+        self.w_mode = _W_MODES[self.cfg.w_mode]
+        self.records = torch.empty(max(n, 1) * nat.REC_DOUBLES, dtype=torch.float64, device=self.dev)
+        self.flags = torch.empty(max(n, 1), dtype=torch.uint8, device=self.dev)
+        self.label_counts = torch.empty(32, dtype=torch.int64, device=self.dev)
+        self.counters = torch.empty(nat.NCOUNTERS, dtype=torch.int64, device=self.dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.cap = max(1 << 20, 8 * n)
+        self._ws = {}
+        self._img = {}
+        self.lib = nat.load()
+
+    def lr(self) -> float:
+        return polylr(self.step_count, self.total_steps, self.base_lr)
+
+    def _workspace(self, w, h):
+        import torch
+        key = (w, h, self.cap)
+        ws = self._ws.get(key)
+        if ws is None:
+            nbytes = self.lib.g6r_backward_workspace_bytes(self.n, w, h, 16, self.cap)
+            self._ws = {}   # one live size at a time (caps only grow)
+            ws = self._ws[key] = (torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.dev),
+                                  nbytes)
+        return ws
+
+    def _buffers(self, w, h):
+        import torch
+        b = self._img.get((w, h))
+        if b is None:
+            b = self._img[(w, h)] = (torch.empty((h, w, 4), dtype=torch.float64, device=self.dev),
+                                     torch.empty((h, w, 4), dtype=torch.float64, device=self.dev))
+        return b
+
+    def _prepare(self):
+        from .raster import ScenePrep
+        p = self.params
+        nat.check(self.lib.g6r_prepare(
+            self.n, _ptr(p["mu_p"]), _ptr(p["mu_d"]), _ptr(p["cov_raw"]), _ptr(p["sh"]),
+            _ptr(p["opacity_raw"]), _ptr(self.labels), ctypes.cast(self.ss, ctypes.c_void_p),
+            self.directional_scale, self.w_mode, _ptr(self.records), _ptr(self.flags),
+            _ptr(self.label_counts), _stream_handle()))
+        prep = ScenePrep(self.records, self.flags, self.label_counts.cpu().numpy(), self.n,
+                         self.cfg.w_mode, self.dev)
+        _selection(prep, None, self.cfg, RenderStats())   # degenerate policy (raster.py:431-440)
+        return prep
+
+    def step(self, view_index: int) -> dict:
+        """One iteration on view ``view_index``; returns lr, l1, ssim_loss, total."""
+        cam, target = self.views[view_index]
+        w, h = int(cam.width), int(cam.height)
+        prep = self._prepare()
+        sc = prep.scene_struct()
+        camst = _camera_struct(cam)
+        image, gimg = self._buffers(w, h)
+        stream = _stream_handle()
+        while True:
+            ws, nbytes = self._workspace(w, h)
+            nat.check(self.lib.g6r_backward_forward(
+                ctypes.byref(sc), 0xFFFF, ctypes.byref(camst), ctypes.byref(self.ccfg), _ptr(ws),
+                nbytes, self.cap, _ptr(self.counters), _ptr(image), stream))
+            c = self.counters.cpu().numpy()
+            if not c[nat.CNT_OVERFLOW]:
+                break
+            self.cap = min(int(c[nat.CNT_ENTRIES] * 1.25) + 4096, (1 << 30) - 1)
+        lr_now = self.lr()
+        (total, l1, ssim_loss), _ = loss_device(image, target, self.loss_cfg, grad_out=gimg)
+        p, g = self.params, self.grads
+        nat.check(self.lib.g6r_backward_apply(
+            ctypes.byref(sc), ctypes.byref(camst), ctypes.byref(self.ccfg), _ptr(ws), nbytes,
+            self.cap, _ptr(p["mu_p"]), _ptr(p["mu_d"]), _ptr(p["cov_raw"]), _ptr(p["sh"]),
+            ctypes.cast(self.ss, ctypes.c_void_p), self.directional_scale, self.w_mode,
+            _ptr(gimg), *[_ptr(g[k]) for k in PARAM_GROUPS], _ptr(self.counters), stream))
+        self._adam()
+        return {"lr": lr_now, "l1": l1, "ssim_loss": ssim_loss, "total": total}
+
+    def _adam(self):
+        self.flag.zero_()
+        stream = _stream_handle()
+        for k in PARAM_GROUPS:
+            nat.check(self.lib.g6r_any_nonfinite(self.params[k].numel(), _ptr(self.grads[k]),
+                                                 _ptr(self.flag), stream))
+        if int(self.flag.item()):
+            self.skipped += 1
+            return
+        lr_now = self.lr()
+        self.step_count += 1
+        t = self.step_count
+        bias1 = 1.0 - ADAM_BETA1 ** t
+        bias2 = 1.0 - ADAM_BETA2 ** t
+        for k in PARAM_GROUPS:
+            nat.check(self.lib.g6r_adam_step(
+                self.params[k].numel(), _ptr(self.params[k]), _ptr(self.grads[k]), _ptr(self.m[k]),
+                _ptr(self.v[k]), lr_now * self.lr_scale.get(k, 1.0), bias1, bias2, stream))
+
+    def result_scene(self):
+        """The optimised parameters as a host scene of the input's type."""
+        arrays = {k: t.cpu().numpy() for k, t in self.params.items()}
+        if not isinstance(self.scene.mu_p, np.ndarray):
+            from .multigpu import DeviceScene
+            s = self.scene
+            return DeviceScene(labels=s.labels, spatial_scale=s.spatial_scale,
+                               directional_scale=s.directional_scale,
+                               **{k: t.clone() for k, t in self.params.items()})
+        return _with_params(self.scene, **arrays)
+
+    def optimizer_state(self) -> OptimizerState:
+        return OptimizerState(m={k: t.cpu().numpy() for k, t in self.m.items()},
+                              v={k: t.cpu().numpy() for k, t in self.v.items()},
+                              step=self.step_count, total_steps=self.total_steps,
+                              base_lr=self.base_lr, lr_scale=dict(self.lr_scale),
+                              skipped=self.skipped)
+
+
+def finetune(scene, views, iters: int = 300, loss_cfg: LossConfig = None,
+             config: RenderConfig = None, seed: int = 0, base_lr: float = 1e-3,
+             lr_scale: dict = None, trace_path=None, checkpoint_path=None):
+    """Optimise every per-Gaussian parameter against ``views`` on the GPU
+    (diffrender.py:548-585): each iteration samples one (camera, target) pair
+    with ``default_rng(seed)``, renders in f64, backpropagates the photometric
+    loss and applies one Adam step under polynomial lr decay.  Returns
+    ``(scene, history)``; history rows carry iteration, lr, l1, ssim_loss and
+    total.  Deterministic: repeated runs are bit-identical."""
+    if len(views) == 0:
+        raise InvalidParameterError("finetune needs at least one view")
+    if iters < 0:
+        raise InvalidParameterError(f"iters must be non-negative, got {iters}")
+    tr = DeviceTrainer(scene, views, loss_cfg, config, total_steps=max(iters, 1),
+                       base_lr=base_lr, lr_scale=lr_scale)
+    rng = np.random.default_rng(seed)
+    history = []
+    for it in range(iters):
+        row = tr.step(int(rng.integers(len(views))))
+        history.append({"iteration": it, **row})
+    out = tr.result_scene()
+    if trace_path is not None:
+        write_trace(history, trace_path)
+    if checkpoint_path is not None:
+        save_checkpoint(out, tr.optimizer_state(), checkpoint_path)
+    return out, history

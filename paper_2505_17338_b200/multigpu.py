@@ -27,7 +27,7 @@ class DeviceScene:
     nothing and prepares straight from these tensors."""
 
     def __init__(self, mu_p, mu_d, cov_raw, sh, opacity_raw, labels, spatial_scale,
-                 directional_scale):
+                 directional_scale, spacing=None, origin=None, direction=None):
         self.mu_p = mu_p
         self.mu_d = mu_d
         self.cov_raw = cov_raw
@@ -36,9 +36,21 @@ class DeviceScene:
         self.labels = labels
         self.spatial_scale = np.asarray(spatial_scale, dtype=np.float64)
         self.directional_scale = float(directional_scale)
+        self.spacing = np.ones(3) if spacing is None else np.asarray(spacing, np.float64)
+        self.origin = np.zeros(3) if origin is None else np.asarray(origin, np.float64)
+        self.direction = np.eye(3) if direction is None else np.asarray(direction, np.float64)
 
     def __len__(self):
         return int(self.mu_p.shape[0])
+
+    def to_host(self):
+        """Host ``Scene`` with the same parameters (one D2H copy per array)."""
+        from .scene import Scene
+        return Scene(mu_p=self.mu_p.cpu().numpy(), mu_d=self.mu_d.cpu().numpy(),
+                     cov_raw=self.cov_raw.cpu().numpy(), sh=self.sh.cpu().numpy(),
+                     opacity_raw=self.opacity_raw.cpu().numpy(), labels=self.labels.cpu().numpy(),
+                     spacing=self.spacing, origin=self.origin, direction=self.direction,
+                     spatial_scale=self.spatial_scale, directional_scale=self.directional_scale)
 
 
 def shard_views(n_views: int, world: int, rank: int) -> range:

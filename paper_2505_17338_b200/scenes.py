@@ -204,3 +204,18 @@ def orbit_camera(azimuth=0.0, elevation=0.0, distance=70.0, width=64, height=64,
     ca, sa = math.cos(azimuth), math.sin(azimuth)
     position = target + distance * np.array([sa * ce, se, ca * ce])
     return make_camera(position, target, fov_y=fov_y, width=width, height=height)
+
+
+def synthetic_target(width, height, seed=0, channels=4) -> np.ndarray:
+    """A smooth (H, W, channels) f64 target image for fine-tune runs and tests.
+
+    Polynomial in the pixel coordinates with seeded coefficients: only +, -, *
+    so it regenerates bit for bit on any host (no transcendental ufuncs)."""
+    c = np.random.default_rng(seed).uniform(0.05, 0.45, (3, 4))
+    u = (np.arange(width, dtype=np.float64) + 0.5) / width
+    v = (np.arange(height, dtype=np.float64) + 0.5) / height
+    u, v = np.meshgrid(u, v)
+    img = np.ones((height, width, channels))
+    for k in range(3):
+        img[:, :, k] = c[k, 0] + c[k, 1] * u + c[k, 2] * v * v + c[k, 3] * u * v * (1.0 - u)
+    return img

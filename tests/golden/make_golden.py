@@ -19,6 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
 
 from splatct import raster  # noqa: E402  (the reference)
 from splatct.priming import Scene as RefScene  # noqa: E402
@@ -131,7 +132,56 @@ def make_expf():
     np.savez_compressed(os.path.join(HERE, "expf_glibc.npz"), x=x, y=y)
 
 
+from train_cases import FINETUNE_CASES, LOSS_CASES, loss_images  # noqa: E402
+
+
+def make_loss():
+    """Reference _loss_parts (diffrender.py:117-138) on seeded images; stores
+    the scalars, the full gradient for small cases and a seeded sample of
+    gradient entries plus per-channel sums for the large ones."""
+    from splatct.diffrender import LossConfig, _loss_parts
+    out = {}
+    for i, (name, h, w, tc, kw) in enumerate(LOSS_CASES):
+        p, g = loss_images(700 + i, h, w, tc)
+        total, l1, ssim_loss, grad = _loss_parts(p, g, LossConfig(**kw))
+        idx = np.random.default_rng(900 + i).choice(grad.size, min(grad.size, 4096), replace=False)
+        out[f"{name}_parts"] = np.array([total, l1, ssim_loss])
+        out[f"{name}_idx"] = idx
+        out[f"{name}_grad_sample"] = grad.reshape(-1)[idx]
+        out[f"{name}_grad_sums"] = grad.sum(axis=(0, 1))
+        out[f"{name}_grad_abs"] = np.abs(grad).sum(axis=(0, 1))
+        print("loss", name, total, l1, ssim_loss)
+    np.savez_compressed(os.path.join(HERE, "loss.npz"), **out)
+
+
+def make_finetune():
+    """Reference finetune (diffrender.py:548-585) on a fixture scene against
+    synthetic_target views: history rows and the final parameters."""
+    from splatct.diffrender import finetune
+    for name, fixture, views, iters, seed, kw in FINETUNE_CASES:
+        z = np.load(os.path.join(HERE, f"{fixture}.npz"))
+        s = RefScene(mu_p=z["mu_p"], mu_d=z["mu_d"], cov_raw=z["cov_raw"], sh=z["sh"],
+                     opacity_raw=z["opacity_raw"], labels=z["labels"], spacing=np.ones(3),
+                     origin=np.zeros(3), direction=np.eye(3), spatial_scale=z["spatial_scale"],
+                     directional_scale=float(z["directional_scale"]))
+        pairs = []
+        for k, (az, el, w, h) in enumerate(views):
+            cam = scenes.orbit_camera(azimuth=az, elevation=el, width=w, height=h)
+            pairs.append((cam, scenes.synthetic_target(w, h, seed=k)))
+        out, hist = finetune(s, pairs, iters=iters, seed=seed, **kw)
+        np.savez_compressed(
+            os.path.join(HERE, f"ft_{name}.npz"),
+            history=np.array([[r["iteration"], r["lr"], r["l1"], r["ssim_loss"], r["total"]]
+                              for r in hist]),
+            **{k: getattr(out, k) for k in ("mu_p", "mu_d", "cov_raw", "sh", "opacity_raw")})
+        print("finetune", name, hist[-1])
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "train":
+        make_loss()
+        make_finetune()
+        sys.exit(0)
     only_bwd = len(sys.argv) > 1 and sys.argv[1] == "backward"
     if not only_bwd:
         for case in CASES:

@@ -229,3 +229,85 @@ def test_pack_unpack_scene_roundtrip():
         np.testing.assert_array_equal(getattr(ds, f).numpy(), getattr(s, f))
     np.testing.assert_array_equal(ds.spatial_scale, s.spatial_scale)
     assert len(ds) == 33
+
+
+def test_scene_file_roundtrip_and_format_errors(tmp_path):
+    from paper_2505_17338_b200 import sceneio
+    s = scenes.random_scene(np.random.default_rng(4), 257)
+    p = tmp_path / "a.g6ds"
+    sceneio.save_scene(s, p)
+    assert p.stat().st_size == 16 + 152 + 257 * 168
+    t = sceneio.load_scene(p)
+    for k in ("mu_p", "mu_d", "cov_raw", "sh", "opacity_raw"):
+        np.testing.assert_array_equal(getattr(t, k), getattr(s, k).astype(np.float32).astype(np.float64))
+    np.testing.assert_array_equal(t.labels, s.labels)
+    sceneio.save_scene(t, tmp_path / "b.g6ds")   # load-save-load is bit-stable
+    assert (tmp_path / "b.g6ds").read_bytes() == p.read_bytes()
+    blob = p.read_bytes()
+    for bad, msg in ((b"XXXX" + blob[4:], "magic"), (blob[:4] + b"\x02" + blob[5:], "version"),
+                     (blob[:-1], "payload"), (blob[:20], "short")):
+        (tmp_path / "c.g6ds").write_bytes(bad)
+        with pytest.raises(sceneio.SceneFormatError, match=msg):
+            sceneio.load_scene(tmp_path / "c.g6ds")
+
+
+def test_scene_file_bytes_match_reference_writer(ref, tmp_path):
+    from splatct import sceneio as RS
+    from splatct.priming import Scene as RScene
+    from paper_2505_17338_b200 import sceneio
+    s = scenes.random_scene(np.random.default_rng(8), 100)
+    rs = RScene(mu_p=s.mu_p, mu_d=s.mu_d, cov_raw=s.cov_raw, sh=s.sh, opacity_raw=s.opacity_raw,
+                labels=s.labels, spacing=np.array([1.5, 1.5, 2.0]), origin=np.array([1.0, 2, 3]),
+                direction=np.eye(3)[[1, 0, 2]], spatial_scale=np.array([0.5, 1.0, 2.0]),
+                directional_scale=0.7)
+    RS.save_scene(rs, tmp_path / "r.g6ds")
+    sceneio.save_scene(rs, tmp_path / "m.g6ds")
+    assert (tmp_path / "r.g6ds").read_bytes() == (tmp_path / "m.g6ds").read_bytes()
+    t = sceneio.load_scene(tmp_path / "r.g6ds")
+    np.testing.assert_array_equal(t.direction, rs.direction)
+    assert t.directional_scale == 0.7
+
+
+def test_loss_config_and_polylr_match_reference_rules():
+    from paper_2505_17338_b200 import diffrender as D
+    c = D.LossConfig()
+    assert abs(sum(c.ms_ssim_weights) - 1.0) < 1e-15
+    for kw in (dict(lambda_l1=-1.0), dict(lambda_l1=0.0, lambda_ssim=0.0), dict(ms_ssim_scales=0),
+               dict(ms_ssim_scales=2), dict(ms_ssim_weights=(1, 1, 1, 1, 0))):
+        with pytest.raises(InvalidParameterError):
+            D.LossConfig(**kw)
+    assert D.polylr(0, 10, 1e-3) == 1e-3
+    assert D.polylr(10, 10, 1e-3) == 0.0
+    assert D.polylr(3, 10, 2e-3) == 2e-3 * (1.0 - 3 / 10) ** 0.9
+    with pytest.raises(InvalidParameterError):
+        D.polylr(11, 10, 1e-3)
+    with pytest.raises(InvalidParameterError):
+        D.finetune(scenes.random_scene(np.random.default_rng(0), 3), [])
+
+
+def test_train_entry_points_reject_bad_arguments():
+    import ctypes
+    lib = nat.load()
+    parts = (ctypes.c_double * 3)()
+    w = (ctypes.c_double * 5)(*([0.2] * 5))
+    # null pointers, bad channel count, tiny image, bad scales: rejected on the host
+    assert lib.g6r_loss_grad(None, None, 3, 64, 64, 0.8, 0.2, 5, w, None, 0, None, parts,
+                             None) == nat.G6R_EINVAL
+    dummy = ctypes.c_void_p(256)
+    assert lib.g6r_loss_grad(dummy, dummy, 2, 64, 64, 0.8, 0.2, 5, w, dummy, 1 << 30, dummy,
+                             parts, None) == nat.G6R_EINVAL
+    assert lib.g6r_loss_grad(dummy, dummy, 3, 8, 64, 0.8, 0.2, 5, w, dummy, 1 << 30, dummy,
+                             parts, None) == nat.G6R_EINVAL
+    assert lib.g6r_loss_grad(dummy, dummy, 3, 64, 64, 0.8, 0.2, 6, w, dummy, 1 << 30, dummy,
+                             parts, None) == nat.G6R_EINVAL
+    assert lib.g6r_loss_grad(dummy, dummy, 3, 64, 64, 0.8, 0.2, 5, w, dummy, 16, dummy,
+                             parts, None) == nat.G6R_EINVAL
+    assert lib.g6r_loss_workspace_bytes(64, 64) > 64 * 64 * 8 * 20
+    assert lib.g6r_loss_workspace_bytes(0, 64) == 0
+    assert lib.g6r_adam_step(-1, None, None, None, None, 1e-3, 0.1, 0.001, None) == nat.G6R_EINVAL
+    assert lib.g6r_adam_step(0, None, None, None, None, 1e-3, 0.1, 0.001, None) == nat.G6R_OK
+    assert lib.g6r_any_nonfinite(-1, None, None, None) == nat.G6R_EINVAL
+    assert lib.g6r_decode_records(-1, None, None, None, None, None, None, None, None,
+                                  None) == nat.G6R_EINVAL
+    assert lib.g6r_decode_records(4, ctypes.c_void_p(257), dummy, dummy, dummy, dummy, dummy,
+                                  dummy, dummy, None) == nat.G6R_EINVAL

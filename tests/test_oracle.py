@@ -20,7 +20,8 @@ from paper_2505_17338_b200.scene import Scene
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-               if not p.endswith("expf_glibc.npz") and not os.path.basename(p).startswith("bwd_"))
+               if os.path.basename(p)[:-4] not in ("expf_glibc", "loss")
+               and not os.path.basename(p).startswith(("bwd_", "ft_")))
 
 
 def load_case(name):
@@ -111,3 +112,17 @@ def test_oracle_backward_matches_reference_kernel(oracle, ref):
                                     en.tile_starts, en.tiles_x, 16, cam.width, cam.height,
                                     st.final_t, st.last_contrib, g)
     np.testing.assert_array_equal(got, want)
+
+
+def test_loss_oracle_matches_golden(oracle):
+    """oracle.loss_parts against the reference's _loss_parts (tests/golden/loss.npz)."""
+    from train_cases import LOSS_CASES, loss_images, oracle_kwargs
+    z = np.load(os.path.join(GOLDEN, "loss.npz"))
+    for i, (name, h, w, tc, kw) in enumerate(LOSS_CASES):
+        p, g = loss_images(700 + i, h, w, tc)
+        total, l1, ssim_loss, grad = oracle.loss_parts(p, g, **oracle_kwargs(kw))
+        np.testing.assert_allclose([total, l1, ssim_loss], z[f"{name}_parts"], rtol=1e-13, atol=1e-15)
+        gs = grad.reshape(-1)[z[f"{name}_idx"]]
+        np.testing.assert_allclose(gs, z[f"{name}_grad_sample"], rtol=1e-9,
+                                   atol=1e-12 * np.abs(gs).max())
+        np.testing.assert_allclose(np.abs(grad).sum(axis=(0, 1)), z[f"{name}_grad_abs"], rtol=1e-10)
