@@ -232,6 +232,39 @@ int g6r_decode_records(int64_t n, const void *records, double *mu_p, double *mu_
                        double *cov_raw, double *sh, double *opacity_raw, uint8_t *labels,
                        int32_t *bad, g6r_stream_t stream);
 
+/* Order-preserving stream compaction scratch for n items (Psi decode over
+ * the half-grid voxels, group filter over scene rows). */
+size_t g6r_compact_workspace_bytes(int64_t n);
+
+/* Psi decode (priming.py:232-285 decode_param_volume) in two calls: count the
+ * foreground voxels of the half grid (dims = D', H', W'; labels_half (V) u8 =
+ * labels[::2, ::2, ::2][:D', :H', :W']), writing *count (device int64) and the
+ * per-chunk offsets into the workspace; the caller sizes the outputs, then
+ * decode emits the scene rows in np.nonzero order.  psi is (37, V) f32
+ * (psi_f32=1, the .raw file precision) or f64; base_rgba (4, V) f64 are input
+ * channels 2..5 on the half grid; spacing, origin (3) and direction (3x3,
+ * row-major) are host arrays.  Outputs as the scene SoA: (count,3) (count,3)
+ * (count,21) (count,12) (count) and labels (count). */
+int g6r_decode_param_volume_count(const int32_t *dims /* host (3) */, const uint8_t *labels_half,
+                                  void *workspace, size_t workspace_bytes, int64_t *count,
+                                  g6r_stream_t stream);
+int g6r_decode_param_volume(const int32_t *dims /* host (3) */, const void *psi, int32_t psi_f32,
+                            const double *base_rgba, const uint8_t *labels_half,
+                            const double *spacing, const double *origin, const double *direction,
+                            void *workspace, size_t workspace_bytes, double *mu_p, double *mu_d,
+                            double *cov_raw, double *sh, double *opacity_raw, uint8_t *labels,
+                            g6r_stream_t stream);
+
+/* Group filter (priming.py:362-374 filter_scene): rows whose label bit is set
+ * in group_mask, in scene order, into outputs of capacity n; *count (device
+ * int64) receives the kept row count. */
+int g6r_filter_rows(int64_t n, const uint8_t *labels, uint32_t group_mask, const double *mu_p,
+                    const double *mu_d, const double *cov_raw, const double *sh,
+                    const double *opacity_raw, void *workspace, size_t workspace_bytes,
+                    double *out_mu_p, double *out_mu_d, double *out_cov_raw, double *out_sh,
+                    double *out_opacity_raw, uint8_t *out_labels, int64_t *count,
+                    g6r_stream_t stream);
+
 /* Photometric loss lambda_l1 * L1 + lambda_ssim * (1 - MS-SSIM) on the RGB
  * channels and its gradient with respect to the rendered image
  * (diffrender.py:117-138 _loss_parts, _ssim.py:123-201 ms_ssim_with_grad).

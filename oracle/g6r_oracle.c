@@ -269,6 +269,14 @@ void or_expf_glibc_batch(int64_t n, const float *x, float *y)
     for (int64_t i = 0; i < n; ++i) y[i] = or_expf_glibc(x[i]);
 }
 
+/* out[i] = fma(a[i], b[i], c[i]), correctly rounded (C99 fma).  The reference's
+ * (N,3) @ (3,3) world-coordinate matmul (priming.py:134) runs through OpenBLAS
+ * dgemm, which on the reference host accumulates fma(q2,d2, fma(q1,d1, q0*d0)). */
+void or_fma_batch(int64_t n, const double *a, const double *b, const double *c, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = fma(a[i], b[i], c[i]);
+}
+
 DEFINE_COMPOSITE(or_composite_f32, float, expf)
 DEFINE_COMPOSITE(or_composite_f64, double, exp)
 

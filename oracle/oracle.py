@@ -66,6 +66,7 @@ def lib():
             getattr(L, name).argtypes = [P, P, P, P, P, P, I64, I, I, I, I, P, P, P]
         L.or_composite_backward.argtypes = [P, P, P, P, P, P, I64, I, I, I, I, P, P, P, P]
         L.or_expf_glibc_batch.argtypes = [I64, P, P]
+        L.or_fma_batch.argtypes = [I64, P, P, P, P]
         _lib = L
     return _lib
 
@@ -510,3 +511,41 @@ def loss_parts(pred, gt, lambda_l1=0.8, lambda_ssim=0.2, scales=5,
         grad_rgb = grad_rgb - lambda_ssim * gm
     grad[:, :, :3] = grad_rgb
     return lambda_l1 * l1 + lambda_ssim * ssim_loss, l1, ssim_loss, grad
+
+
+# ---------------------------------------------------------------------------
+# Scene ingest: Psi decode (priming.py:232-285), restated
+# ---------------------------------------------------------------------------
+
+def fma(a, b, c):
+    """Correctly rounded a*b + c, broadcast (C99 fma via g6r_oracle.c)."""
+    a, b, c = np.broadcast_arrays(np.asarray(a, np.float64), np.asarray(b, np.float64),
+                                  np.asarray(c, np.float64))
+    a, b, c = (np.ascontiguousarray(x) for x in (a, b, c))
+    out = np.empty_like(a)
+    lib().or_fma_batch(a.size, _p(a), _p(b), _p(c), _p(out))
+    return out
+
+
+def decode_param_volume(psi, in6_channels, labels, spacing, origin, direction):
+    """Scene rows (dict of arrays) for the foreground of the half grid.  World
+    coordinates as origin + fma(q2, d[k,2], fma(q1, d[k,1], q0*d[k,0])) with
+    q = index*2*spacing: the accumulation OpenBLAS dgemm performs for the
+    reference's ``(index * spacing) @ direction.T`` (priming.py:134) on the
+    reference host, pinned by tests/golden/ingest_rotated.npz."""
+    psi = np.asarray(psi, np.float64)
+    dp, hp, wp = psi.shape[1:]
+    lab = np.asarray(labels)[::2, ::2, ::2][:dp, :hp, :wp]
+    base = np.asarray(in6_channels, np.float64)[:, ::2, ::2, ::2][:, :dp, :hp, :wp]
+    zi, yi, xi = np.nonzero(lab)
+    q = np.stack([xi * 2, yi * 2, zi * 2], axis=1).astype(np.float64) * np.asarray(spacing, np.float64)
+    d = np.asarray(direction, np.float64)
+    mu_p = np.asarray(origin, np.float64) + fma(q[:, 2:3], d[:, 2], fma(q[:, 1:2], d[:, 1],
+                                                                       q[:, 0:1] * d[:, 0]))
+    pred = psi[:, zi, yi, xi]
+    sh = np.empty((zi.size, 12))
+    sh[:, :3] = (base[2:5, zi, yi, xi].T - 0.5) / SH_C0 + pred[3:6].T
+    sh[:, 3:] = pred[6:15].T
+    return dict(mu_p=mu_p, mu_d=np.array([0.0, 0.0, 1.0]) + pred[0:3].T,
+                cov_raw=np.ascontiguousarray(pred[16:37].T), sh=sh,
+                opacity_raw=base[5, zi, yi, xi] + pred[15], labels=lab[zi, yi, xi])

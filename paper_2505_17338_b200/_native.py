@@ -98,6 +98,12 @@ _SIGS = {
     "g6r_backward_apply": (ctypes.c_int, [P, P, P, P, SZ, I64, P, P, P, P, P, D, I32, P, P, P, P,
                                           P, P, P, P]),
     "g6r_decode_records": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
+    "g6r_compact_workspace_bytes": (SZ, [I64]),
+    "g6r_decode_param_volume_count": (ctypes.c_int, [P, P, P, SZ, P, P]),
+    "g6r_decode_param_volume": (ctypes.c_int, [P, P, I32, P, P, P, P, P, P, SZ, P, P, P, P, P, P,
+                                               P]),
+    "g6r_filter_rows": (ctypes.c_int, [I64, P, U32, P, P, P, P, P, P, SZ, P, P, P, P, P, P, P,
+                                       P]),
     "g6r_loss_workspace_bytes": (SZ, [I32, I32]),
     "g6r_loss_grad": (ctypes.c_int, [P, P, I32, I32, I32, D, D, I32, P, P, SZ, P, P, P]),
     "g6r_adam_step": (ctypes.c_int, [I64, P, P, P, P, D, D, D, P]),

@@ -534,6 +534,77 @@ int g6r_decode_records(int64_t n, const void *records, double *mu_p, double *mu_
     return G6R_OK;
 }
 
+size_t g6r_compact_workspace_bytes(int64_t n) { return compact_workspace_bytes(n); }
+
+int g6r_decode_param_volume_count(const int32_t *dims, const uint8_t *labels_half, void *workspace,
+                                  size_t workspace_bytes, int64_t *count, g6r_stream_t stream) {
+    if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(G6R_EINVAL, "psi decode: dims must be positive");
+    const int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
+    if (!labels_half || !count || !workspace) return fail(G6R_EINVAL, "psi decode: null pointer");
+    if (workspace_bytes < compact_workspace_bytes(V))
+        return fail(G6R_EINVAL, "psi decode: workspace too small");
+    if (launch_decode_count(V, labels_half, workspace, count, (cudaStream_t)stream))
+        return cuda_check("decode_count");
+    return G6R_OK;
+}
+
+int g6r_decode_param_volume(const int32_t *dims, const void *psi, int32_t psi_f32,
+                            const double *base_rgba, const uint8_t *labels_half,
+                            const double *spacing, const double *origin, const double *direction,
+                            void *workspace, size_t workspace_bytes, double *mu_p, double *mu_d,
+                            double *cov_raw, double *sh, double *opacity_raw, uint8_t *labels,
+                            g6r_stream_t stream) {
+    if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(G6R_EINVAL, "psi decode: dims must be positive");
+    if (!psi || !base_rgba || !labels_half || !spacing || !origin || !direction || !workspace ||
+        !mu_p || !mu_d || !cov_raw || !sh || !opacity_raw || !labels)
+        return fail(G6R_EINVAL, "psi decode: null pointer");
+    DecodeArgsHost h{};
+    h.V = (int64_t)dims[0] * dims[1] * dims[2];
+    if (workspace_bytes < compact_workspace_bytes(h.V))
+        return fail(G6R_EINVAL, "psi decode: workspace too small");
+    h.psi = psi;
+    h.psi_f32 = psi_f32 != 0;
+    h.base = base_rgba;
+    h.lab = labels_half;
+    h.dh = dims[1];
+    h.dw = dims[2];
+    for (int k = 0; k < 3; ++k) {
+        h.spacing[k] = spacing[k];
+        h.origin[k] = origin[k];
+    }
+    for (int k = 0; k < 9; ++k) h.dir[k] = direction[k];
+    h.mu_p = mu_p;
+    h.mu_d = mu_d;
+    h.cov_raw = cov_raw;
+    h.sh = sh;
+    h.opacity_raw = opacity_raw;
+    h.labels = labels;
+    if (launch_decode_emit(h, workspace, (cudaStream_t)stream)) return cuda_check("decode_emit");
+    return G6R_OK;
+}
+
+int g6r_filter_rows(int64_t n, const uint8_t *labels, uint32_t group_mask, const double *mu_p,
+                    const double *mu_d, const double *cov_raw, const double *sh,
+                    const double *opacity_raw, void *workspace, size_t workspace_bytes,
+                    double *out_mu_p, double *out_mu_d, double *out_cov_raw, double *out_sh,
+                    double *out_opacity_raw, uint8_t *out_labels, int64_t *count,
+                    g6r_stream_t stream) {
+    if (n < 0) return fail(G6R_EINVAL, "filter: n must be >= 0");
+    if (!count || !workspace) return fail(G6R_EINVAL, "filter: null pointer");
+    if (n && (!labels || !mu_p || !mu_d || !cov_raw || !sh || !opacity_raw || !out_mu_p ||
+              !out_mu_d || !out_cov_raw || !out_sh || !out_opacity_raw || !out_labels))
+        return fail(G6R_EINVAL, "filter: null pointer");
+    if (workspace_bytes < compact_workspace_bytes(n)) return fail(G6R_EINVAL, "filter: workspace too small");
+    const double *in[5] = {mu_p, mu_d, cov_raw, sh, opacity_raw};
+    double *out[5] = {out_mu_p, out_mu_d, out_cov_raw, out_sh, out_opacity_raw};
+    if (launch_filter_rows(n, labels, group_mask, in, out, out_labels, workspace, count,
+                           (cudaStream_t)stream))
+        return cuda_check("filter_rows");
+    return G6R_OK;
+}
+
 size_t g6r_loss_workspace_bytes(int32_t width, int32_t height) {
     if (width <= 0 || height <= 0) return 0;
     return loss_workspace_bytes(height, width);

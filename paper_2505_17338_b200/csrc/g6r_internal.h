@@ -118,6 +118,25 @@ int sort_passes(int tiles);   // upper bound on radix passes for `tiles` tiles
 // branch per launch).
 void trace_mark(const char *label, cudaStream_t st);
 
+// scene ingest (g6r_ingest.cu)
+struct DecodeArgsHost {
+    const void *psi;
+    int psi_f32;
+    const double *base;
+    const uint8_t *lab;
+    int64_t V;
+    int dh, dw;
+    double spacing[3], origin[3], dir[9];
+    double *mu_p, *mu_d, *cov_raw, *sh, *opacity_raw;
+    uint8_t *labels;
+};
+size_t compact_workspace_bytes(int64_t n);
+int launch_decode_count(int64_t V, const uint8_t *lab, void *ws, int64_t *count, cudaStream_t st);
+int launch_decode_emit(const DecodeArgsHost &h, void *ws, cudaStream_t st);
+int launch_filter_rows(int64_t n, const uint8_t *lab, uint32_t mask, const double *const in[5],
+                       double *const out[5], uint8_t *labels, void *ws, int64_t *count,
+                       cudaStream_t st);
+
 // fine-tune loop (g6r_train.cu)
 size_t loss_workspace_bytes(int h, int w);
 int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,

@@ -12,3 +12,11 @@ class DegenerateCovarianceError(ArithmeticError):
 
 class DegenerateGeometryError(ValueError):
     """Geometric construction is undefined (e.g. zero-length direction)."""
+
+
+class VolumeFormatError(ValueError):
+    """Volume or parameter-volume shape/file inconsistency (volume.py:67)."""
+
+
+class EmptySceneError(ValueError):
+    """No foreground voxels to instantiate Gaussians from (priming.py:46)."""

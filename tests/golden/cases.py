@@ -1,4 +1,4 @@
-"""Fine-tune loop fixture definitions shared by make_golden.py (which runs the
+"""Fixture definitions (fine-tune loop, scene ingest) shared by make_golden.py (which runs the
 reference here) and the tests (which run anywhere): inputs regenerate from
 seeds, so only the reference's outputs are stored."""
 
@@ -32,3 +32,27 @@ FINETUNE_CASES = [
     ("small", "rand400", [(-0.8, 0.2, 64, 48), (0.7, -0.1, 64, 48)], 20, 3, {}),
     ("ms", "rand400", [(-0.8, 0.2, 192, 180)], 3, 4, dict(base_lr=5e-3)),
 ]
+
+
+# Psi decode (priming.py:232-285): full-resolution dims, seed; inputs regenerate
+# from default_rng(seed) via ingest_inputs
+INGEST_CASES = [("identity", (22, 18, 20), 31, False), ("rotated", (17, 24, 14), 32, True)]
+
+
+def ingest_inputs(dims, seed, rotated):
+    """(psi (37, D/2, H/2, W/2) f64 rounded through f32, in6 channels (6, D, H, W),
+    consolidated labels (D, H, W) u8 with ~30% foreground, spacing, origin, direction)."""
+    rng = np.random.default_rng(seed)
+    d, h, w = dims
+    labels = np.where(rng.uniform(size=dims) < 0.3, rng.integers(1, 12, size=dims), 0).astype(np.uint8)
+    in6 = rng.uniform(0.0, 1.0, (6,) + dims)
+    in6[5] = np.clip(in6[5], 0.05, 0.95)
+    psi = rng.normal(0.0, 0.3, (37, d // 2, h // 2, w // 2)).astype(np.float32).astype(np.float64)
+    spacing = np.array([0.8, 1.25, 2.0])
+    origin = np.array([-10.0, 3.5, 7.25])
+    if rotated:
+        c, s = 0.6, 0.8   # exact in binary: rotation about y with cos 0.6, sin 0.8
+        direction = np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+    else:
+        direction = np.eye(3)
+    return psi, in6, labels, spacing, origin, direction

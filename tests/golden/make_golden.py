@@ -132,7 +132,7 @@ def make_expf():
     np.savez_compressed(os.path.join(HERE, "expf_glibc.npz"), x=x, y=y)
 
 
-from train_cases import FINETUNE_CASES, LOSS_CASES, loss_images  # noqa: E402
+from cases import FINETUNE_CASES, INGEST_CASES, LOSS_CASES, ingest_inputs, loss_images  # noqa: E402
 
 
 def make_loss():
@@ -177,7 +177,25 @@ def make_finetune():
         print("finetune", name, hist[-1])
 
 
+def make_ingest():
+    """Reference decode_param_volume (priming.py:232-285) on seeded volumes."""
+    from splatct.priming import ParamVolume, decode_param_volume
+    from splatct.volume import InputVolume6, LabelVolume
+    for name, dims, seed, rotated in INGEST_CASES:
+        psi, in6, labels, spacing, origin, direction = ingest_inputs(dims, seed, rotated)
+        s = decode_param_volume(ParamVolume(psi), InputVolume6(in6, spacing, origin, direction),
+                                LabelVolume(labels, consolidated=True))
+        np.savez_compressed(os.path.join(HERE, f"ingest_{name}.npz"),
+                            **{k: getattr(s, k) for k in ("mu_p", "mu_d", "cov_raw", "sh",
+                                                          "opacity_raw", "labels",
+                                                          "spatial_scale")})
+        print("ingest", name, len(s))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "ingest":
+        make_ingest()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "train":
         make_loss()
         make_finetune()

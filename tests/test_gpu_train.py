@@ -19,7 +19,7 @@ from paper_2505_17338_b200 import scenes, sceneio
 from paper_2505_17338_b200.scene import Scene
 
 from test_oracle import GOLDEN
-from train_cases import FINETUNE_CASES, LOSS_CASES, loss_images, oracle_kwargs
+from cases import FINETUNE_CASES, LOSS_CASES, loss_images, oracle_kwargs
 
 pytestmark = pytest.mark.gpu
 

@@ -21,7 +21,7 @@ from paper_2505_17338_b200.scene import Scene
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
                if os.path.basename(p)[:-4] not in ("expf_glibc", "loss")
-               and not os.path.basename(p).startswith(("bwd_", "ft_")))
+               and not os.path.basename(p).startswith(("bwd_", "ft_", "ingest_")))
 
 
 def load_case(name):
@@ -116,7 +116,7 @@ def test_oracle_backward_matches_reference_kernel(oracle, ref):
 
 def test_loss_oracle_matches_golden(oracle):
     """oracle.loss_parts against the reference's _loss_parts (tests/golden/loss.npz)."""
-    from train_cases import LOSS_CASES, loss_images, oracle_kwargs
+    from cases import LOSS_CASES, loss_images, oracle_kwargs
     z = np.load(os.path.join(GOLDEN, "loss.npz"))
     for i, (name, h, w, tc, kw) in enumerate(LOSS_CASES):
         p, g = loss_images(700 + i, h, w, tc)
@@ -126,3 +126,14 @@ def test_loss_oracle_matches_golden(oracle):
         np.testing.assert_allclose(gs, z[f"{name}_grad_sample"], rtol=1e-9,
                                    atol=1e-12 * np.abs(gs).max())
         np.testing.assert_allclose(np.abs(grad).sum(axis=(0, 1)), z[f"{name}_grad_abs"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("case", ["identity", "rotated"])
+def test_decode_oracle_matches_golden(oracle, case):
+    from cases import INGEST_CASES, ingest_inputs
+    (name, dims, seed, rotated), = [c for c in INGEST_CASES if c[0] == case]
+    psi, in6, labels, spacing, origin, direction = ingest_inputs(dims, seed, rotated)
+    got = oracle.decode_param_volume(psi, in6, labels, spacing, origin, direction)
+    z = np.load(os.path.join(GOLDEN, f"ingest_{name}.npz"))
+    for k in ("mu_p", "mu_d", "cov_raw", "sh", "opacity_raw", "labels"):
+        np.testing.assert_array_equal(got[k], z[k], err_msg=k)
