@@ -107,12 +107,17 @@ typedef struct g6r_splat_out {
  * (H,W) int32.  entry_splat (E) / tile_starts (T+1) are optional copies of the
  * sorted tile runs (raster.py:201-208). */
 typedef struct g6r_frame {
-    void *image;
+    void *image;            /* required unless rgba8 is given */
     void *final_t;
     int32_t *last_contrib;
     int64_t *counters;      /* G6R_NCOUNTERS, required */
     int32_t *entry_splat;   /* optional, capacity entry_capacity */
     int64_t *tile_starts;   /* optional, T+1 */
+    /* optional served-frame output fused into the compositor epilogue:
+     * (H,W,4) u8 = round(clip(rgb + background * (1 - alpha), 0, 1) * 255),
+     * alpha 255 (metrics.py:21-25 composite_over, _png.py:21-32 to_rgba_u8). */
+    uint8_t *rgba8;
+    double background[3];
 } g6r_frame;
 
 const char *g6r_version(void);

@@ -219,8 +219,8 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     b.nviews = nviews;
     for (int v = 0; v < nviews; ++v) {
         const g6r_frame *fr = &frames[v];
-        if (!fr->image || !fr->counters)
-            return fail(G6R_EINVAL, "frame outputs image/counters are required");
+        if ((!fr->image && !fr->rgba8) || !fr->counters)
+            return fail(G6R_EINVAL, "frame outputs image (or rgba8) and counters are required");
         if (int rc = make_view(&cams[v], cfg, b.vp[v])) return rc;
         if (b.vp[v].iw != b.vp[0].iw || b.vp[v].ih != b.vp[0].ih)
             return fail(G6R_EINVAL, "views of one batch must share the image size");
@@ -231,7 +231,10 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     for (int v = 0; v < nviews; ++v) {
         b.ws[v] = carve(static_cast<char *>(ws_base) + L.total * v, L, cap);
         b.out[v] = ViewOut{frames[v].image, frames[v].final_t, frames[v].last_contrib,
-                           frames[v].counters, frames[v].entry_splat, frames[v].tile_starts};
+                           frames[v].counters, frames[v].entry_splat, frames[v].tile_starts,
+                           frames[v].rgba8,
+                           {frames[v].background[0], frames[v].background[1],
+                            frames[v].background[2]}};
     }
     if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     prof_mark(prof, 0, st);

@@ -250,11 +250,24 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     }
     if (inside) {
         const int64_t p = (int64_t)py * vp.iw + px;
-        if constexpr (sizeof(Real) == 4) {
-            reinterpret_cast<float4 *>(image)[p] = make_float4(ar, ag, ab, aa);
-        } else {
-            reinterpret_cast<double2 *>(image)[2 * p] = make_double2(ar, ag);
-            reinterpret_cast<double2 *>(image)[2 * p + 1] = make_double2(ab, aa);
+        if (image) {
+            if constexpr (sizeof(Real) == 4) {
+                reinterpret_cast<float4 *>(image)[p] = make_float4(ar, ag, ab, aa);
+            } else {
+                reinterpret_cast<double2 *>(image)[2 * p] = make_double2(ar, ag);
+                reinterpret_cast<double2 *>(image)[2 * p + 1] = make_double2(ab, aa);
+            }
+        }
+        if (uint8_t *q = bt.out[view].rgba8) {
+            // composite_over (metrics.py:24) then to_rgba_u8 (_png.py:30), in f64
+            const double *bg = bt.out[view].bg;
+            const double t = 1.0 - (double)aa;
+            const double c[3] = {(double)ar + bg[0] * t, (double)ag + bg[1] * t,
+                                 (double)ab + bg[2] * t};
+            unsigned char u[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) u[k] = (unsigned char)rint(fmin(fmax(c[k], 0.0), 1.0) * 255.0);
+            reinterpret_cast<uchar4 *>(q)[p] = make_uchar4(u[0], u[1], u[2], 255);
         }
         if (final_t) final_t[p] = T;
         if (last_contrib) last_contrib[p] = last;

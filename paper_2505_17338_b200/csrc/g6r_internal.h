@@ -46,6 +46,8 @@ struct ViewOut {
     int64_t *counters;       // G6R_NCOUNTERS
     int32_t *entry_splat;    // optional copy of the sorted runs
     int64_t *tile_starts;    // optional copy of the tile ranges
+    uint8_t *rgba8;          // optional served frame (composite over bg, quantised)
+    double bg[3];
 };
 
 // One launch's views.  All views share tile size, precision and image size.

@@ -122,7 +122,8 @@ def decode_param_volume_device(psi, in6, labels, device=None):
     lib = nat.load()
     V = int(np.prod(dims))
     with torch.cuda.device(dev):
-        psi_t = torch.from_numpy(np.ascontiguousarray(chans)).to(dev)
+        host = np.ascontiguousarray(chans)
+        psi_t = torch.from_numpy(host if host.flags.writeable else host.copy()).to(dev)
         lab_t = torch.from_numpy(lab).to(dev)
         base_t = torch.from_numpy(base).to(dev)
         nbytes = lib.g6r_compact_workspace_bytes(V)

@@ -511,12 +511,17 @@ DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
 
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
                  capacity: int | None = None, out=None, profiler=None,
-                 concurrency: int = DEFAULT_CONCURRENCY):
+                 concurrency: int = DEFAULT_CONCURRENCY, rgba8=None, background=(0.0, 0.0, 0.0),
+                 image: bool = True):
     """Render ``cameras`` (same size) with up to ``concurrency`` views in flight.
 
     Returns ``(images, counters)``: ``images`` (V,H,W,4) on the device,
     ``counters`` (V,16) int64.  No synchronisation; a view with
-    ``counters[v, 8] != 0`` overflowed ``capacity`` and must be re-rendered."""
+    ``counters[v, 8] != 0`` overflowed ``capacity`` and must be re-rendered.
+    ``rgba8`` ((V,H,W,4) uint8 device tensor) additionally receives the served
+    frame composited over ``background`` and quantised in the compositor's
+    epilogue; with ``image=False`` the float image is not written at all
+    (``images`` is then None)."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cfg = _check_config(config)
@@ -527,7 +532,15 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         raise InvalidParameterError("render_views needs cameras of one image size")
     dt = torch.float32 if config.precision == "f32" else torch.float64
     dev = prep.device
-    images = out if out is not None else torch.empty((V, H, W, 4), dtype=dt, device=dev)
+    if image:
+        images = out if out is not None else torch.empty((V, H, W, 4), dtype=dt, device=dev)
+    elif rgba8 is None:
+        raise InvalidParameterError("image=False needs an rgba8 output")
+    else:
+        images = None
+    if rgba8 is not None and (tuple(rgba8.shape) != (V, H, W, 4) or rgba8.dtype != torch.uint8
+                              or not rgba8.is_contiguous()):
+        raise InvalidParameterError(f"rgba8 must be a contiguous ({V}, {H}, {W}, 4) uint8 tensor")
     counters = torch.empty((V, nat.NCOUNTERS), dtype=torch.int64, device=dev)
     cap = int(capacity or prep.entry_hint)
     slots = max(1, min(int(concurrency), 8, V))
@@ -535,14 +548,17 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
     ws = torch.empty(max(per * slots, 256), dtype=torch.uint8, device=dev)
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
-    frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr(), 0, 0, counters[v].data_ptr(), 0, 0)
+    bg = (ctypes.c_double * 3)(*[float(c) for c in background])
+    frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr() if images is not None else 0, 0, 0,
+                                         counters[v].data_ptr(), 0, 0,
+                                         rgba8[v].data_ptr() if rgba8 is not None else 0, bg)
                                for v in range(V)])
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
                                           _ptr(ws), per * slots, cap, frames, slots,
                                           profiler.handle if profiler is not None else None,
                                           _stream_handle()))
-    images._g6r_keepalive = ws
+    counters._g6r_keepalive = ws
     return images, counters
 
 
@@ -590,6 +606,62 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         fr, _ = _render_checked(prep, bits, cams[v], config, False)
         out[v] = fr.image.cpu().numpy()
     return out
+
+
+def render_frames_u8(scene, cameras, background=(0.0, 0.0, 0.0), group_mask=None,
+                     config: RenderConfig = DEFAULT_CONFIG, batch: int = DEFAULT_CONCURRENCY,
+                     device_out: bool = False):
+    """Served frames: (V, H, W, 4) uint8 RGBA of every view composited over an
+    opaque ``background`` -- exactly ``to_rgba_u8(composite_over(render(scene,
+    cam), background))`` of the reference (metrics.py:21-25, _png.py:21-32) --
+    produced by the compositor's epilogue, so no float image is written to HBM
+    and 1 byte per channel crosses PCIe.  ``device_out`` returns the device
+    tensor instead of a host array."""
+    prep = prepare_scene(scene, config.w_mode)
+    bits = _selection(prep, group_mask, config, RenderStats())
+    cams = list(cameras)
+    V = len(cams)
+    if V == 0:
+        return np.zeros((0, 0, 0, 4), dtype=np.uint8)
+    H, W = int(cams[0].height), int(cams[0].width)
+    dev = prep.device
+    frames = torch.empty((V, H, W, 4), dtype=torch.uint8, device=dev)
+    chunk = max(1, min(int(batch), 8))
+    host = None if device_out else torch.empty((V, H, W, 4), dtype=torch.uint8, pin_memory=True)
+    main = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    counters = []
+    for k in range(0, V, chunk):
+        sl = slice(k, min(V, k + chunk))
+        _, cnt = render_views(scene, cams[sl], group_mask, config, concurrency=chunk,
+                              rgba8=frames[sl], background=background, image=False)
+        counters.append(cnt)
+        if host is not None:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                host[sl].copy_(frames[sl], non_blocking=True)
+                frames[sl].record_stream(copy)
+    cnt = torch.cat(counters).cpu().numpy()   # synchronises the render stream
+    for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
+        while True:   # re-render an overflowed view with a grown capacity
+            prep.entry_hint = min(int(cnt[v, nat.CNT_ENTRIES] * 1.25) + 4096, (1 << 30) - 1)
+            _, c1 = render_views(scene, [cams[v]], group_mask, config, concurrency=1,
+                                 capacity=prep.entry_hint, rgba8=frames[v:v + 1],
+                                 background=background, image=False)
+            c1 = c1.cpu().numpy()
+            if not c1[0, nat.CNT_OVERFLOW]:
+                break
+            cnt[v] = c1[0]
+        if host is not None:
+            copy.wait_stream(main)
+            with torch.cuda.stream(copy):
+                host[v].copy_(frames[v], non_blocking=True)
+    if host is None:
+        return frames
+    copy.synchronize()
+    return host.numpy()
 
 
 def _stats_from_counters(stats: RenderStats, counters) -> None:
