@@ -15,7 +15,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libg6r.so")
+# G6R_LIBRARY overrides the in-tree build (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("G6R_LIBRARY") or os.path.join(HERE, "_lib", "libg6r.so")
 
 G6R_OK = 0
 G6R_EINVAL = -22

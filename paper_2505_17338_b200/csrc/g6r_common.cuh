@@ -65,8 +65,22 @@ struct PayloadF64 {
 // (a dx^2 + c dy^2) <= 4 kappa q, kappa = (a+c)^2 / (4 det); outside the box
 // grown by (1 + delta), delta >> 10 ulp * 4 kappa, the computed power is
 // therefore still < -4.5.  Non-positive-definite conics get an infinite box.
+// Squared-radius bound of the pixels a splat of peak alpha `alpha` can touch:
+// a contribution needs power >= -4.5 (q <= 9) and alpha * exp(power) >= 1/255
+// (q <= 2 ln(255 alpha)); the latter is tighter for alpha < e^4.5 / 255 (~0.35).
+// Margins (1e-5 relative on alpha, 1e-4 absolute on q) cover the float
+// rounding of expf and of the product in the compositor.  Returns a negative
+// value when the splat can never pass the alpha floor.
+__host__ __device__ __forceinline__ double cull_q(double alpha) {
+    const double floor = 1.0 / 255.0;   // <= the f32 compositor's (float)(1/255)
+    const double amax = alpha * (1.0 + 1e-5);
+    if (!(amax > floor)) return -1.0;
+    const double qa = 2.0 * log(amax / floor) + 1e-4;
+    return qa < 9.0 ? qa : 9.0;
+}
+
 __device__ __forceinline__ void cull_extents(double a, double b, double c, double ulp,
-                                             float &ex, float &ey) {
+                                             float &ex, float &ey, double alpha = 1.0) {
     const double det = a * c - b * b;
     if (!(det > 0.0) || !(a > 0.0) || !(c > 0.0)) {
         ex = ey = __int_as_float(0x7f800000);
@@ -78,15 +92,22 @@ __device__ __forceinline__ void cull_extents(double a, double b, double c, doubl
         ex = ey = __int_as_float(0x7f800000);
         return;
     }
+    const double q = cull_q(alpha);
+    if (q < 0.0) {   // can never reach the alpha floor: no pixel box at all
+        ex = ey = __int_as_float(0x7fffffff);
+        return;
+    }
     const double grow = 1.0 + delta;
-    ex = (float)(3.0 * sqrt(c / det) * grow + 1e-3);
-    ey = (float)(3.0 * sqrt(a / det) * grow + 1e-3);
+    const double k = sqrt(q);
+    ex = (float)(k * sqrt(c / det) * grow + 1e-3);
+    ey = (float)(k * sqrt(a / det) * grow + 1e-3);
 }
 
 // Same extents for an f32 conic, in float arithmetic (the determinant exactly
 // from the f32 products in double).  The float evaluation adds at most a few
 // ulp (~1e-6 relative); the extra 1e-5 relative growth absorbs it.
-__device__ __forceinline__ void cull_extents_f32(float a, float b, float c, float &ex, float &ey) {
+__device__ __forceinline__ void cull_extents_f32(float a, float b, float c, float &ex, float &ey,
+                                                 float alpha = 1.0f) {
     const double detd = (double)a * (double)c - (double)b * (double)b;
     const float inf = __int_as_float(0x7f800000);
     if (!(detd > 0.0) || !(a > 0.0f) || !(c > 0.0f)) {
@@ -100,9 +121,15 @@ __device__ __forceinline__ void cull_extents_f32(float a, float b, float c, floa
         ex = ey = inf;
         return;
     }
+    const double q = cull_q((double)alpha);
+    if (q < 0.0) {
+        ex = ey = __int_as_float(0x7fffffff);
+        return;
+    }
     const float grow = 1.0f + delta;
-    ex = 3.0f * sqrtf(c * inv) * grow + 1e-3f;
-    ey = 3.0f * sqrtf(a * inv) * grow + 1e-3f;
+    const float k = (float)sqrt(q) * (1.0f + 1e-6f);
+    ex = k * sqrtf(c * inv) * grow + 1e-3f;
+    ey = k * sqrtf(a * inv) * grow + 1e-3f;
 }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -101,6 +101,76 @@ __device__ __forceinline__ float splat_exp(float x, const unsigned long long *ta
 }
 __device__ __forceinline__ double splat_exp(double x, const unsigned long long *) { return exp(x); }
 
+// Shared-memory reads through 32-bit shared-window addresses held in
+// registers: generic pointers into shared memory make the compiler rebuild the
+// window base (S2R CgaCtaId + LEA) at every use inside the hit loop.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void lds_splat(uint32_t a, Px<float>::S &s) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(s.a.x), "=f"(s.a.y), "=f"(s.a.z), "=f"(s.a.w) : "r"(a));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];"
+                 : "=f"(s.b.x), "=f"(s.b.y), "=f"(s.b.z), "=f"(s.b.w) : "r"(a));
+    asm volatile("ld.shared.f32 %0, [%1+32];" : "=f"(s.c) : "r"(a));
+}
+__device__ __forceinline__ void lds_splat(uint32_t a, Px<double>::S &s) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s.a.x), "=d"(s.a.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(s.b.x), "=d"(s.b.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+32];" : "=d"(s.c.x), "=d"(s.c.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+48];" : "=d"(s.d.x), "=d"(s.d.y) : "r"(a));
+    asm volatile("ld.shared.f64 %0, [%1+64];" : "=d"(s.e) : "r"(a));
+}
+__device__ __forceinline__ unsigned lds_u32(uint32_t a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned long long lds_u64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
+// Operands of the hit loop's expf.  The 64-bit constants live in the constant
+// bank, which DMUL/DFMA read directly (c[bank][offset] operands); as literals
+// ptxas rebuilds them with 32-bit moves on every splat visit.  The table's
+// window address goes through an opaque move for the same reason.
+__constant__ double c_exp_k[4] = {0x1.71547652b82fep+5, 0x1.c6af84b912394p-20,
+                                  0x1.ebfce50fac4f3p-13, 0x1.62e42ff0c52d6p-6};
+struct ExpOperands {
+    uint32_t tab;
+};
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ ExpOperands exp_operands(uint32_t tab) { return ExpOperands{opaque(tab)}; }
+
+// glibc expf (g6r_common.cuh expf_glibc, same operations) with the operands above
+__device__ __forceinline__ float splat_exp_s(float x, const ExpOperands &e) {
+    const double kInvLn2N = c_exp_k[0];
+    const double kShift = 0x1.8p+52;
+    const double c0 = c_exp_k[1], c1 = c_exp_k[2], c2 = c_exp_k[3];
+    const uint32_t tab = e.tab;
+    const double xd = (double)x;
+    const double z = __dmul_rn(kInvLn2N, xd);
+    double kd = __dadd_rn(z, kShift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, kShift);
+    const double r = __fma_rn(kInvLn2N, xd, -kd);
+    const unsigned long long t = lds_u64(tab + 8u * (unsigned)(ki & 31ull)) + (ki << 47);
+    const double s = __longlong_as_double((long long)t);
+    const double p = __fma_rn(c0, r, c1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(c2, r, 1.0);
+    y = __fma_rn(p, r2, y);
+    y = __dmul_rn(y, s);
+    return __double2float_rn(y);
+}
+__device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { return exp(x); }
+
 // One CTA per tile, one thread per pixel.  kNB > 0: compile-time block size
 // (16x16 tiles, static shared memory); kNB == 0: any tile size up to 32x32.
 //
@@ -135,6 +205,8 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float4 s_wbox[32];   // pixel-centre box per warp
     if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
+    const uint32_t sp_base = smem_addr(sp), mask_base = smem_addr(smask);
+    const ExpOperands eops = exp_operands(smem_addr(s_tab));
 
     const int ts = vp.tile_size;
     const int tile = blockIdx.x;
@@ -205,8 +277,8 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         const int64_t e1 = b0 + nb + threadIdx.x;
         const bool have1 = e1 < hi;
         if (have1) pre = payload[vals[e1]];
-        const S *bsp = sp + buf * nb;
-        const unsigned *bmask = smask + buf * nb;
+        const uint32_t bsp = sp_base + (uint32_t)(buf * nb) * (uint32_t)sizeof(S);
+        const uint32_t bmask = mask_base + (uint32_t)(buf * nb) * 4u;
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
         if (!__all_sync(wmask, done)) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
@@ -214,21 +286,22 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                 for (int k = 0; k < 32; k += wlanes) {
                     const int jl = c0 + k + lane;
                     const unsigned b = __ballot_sync(
-                        wmask, lane + k < 32 && jl < cnt && ((bmask[jl] >> warp) & 1u));
+                        wmask, lane + k < 32 && jl < cnt && ((lds_u32(bmask + 4u * jl) >> warp) & 1u));
                     hits |= b << k;
                 }
                 while (hits) {
                     const int j = c0 + __ffs(hits) - 1;
                     hits &= hits - 1;
                     if (done) continue;
-                    const S s = bsp[j];
+                    S s;
+                    lds_splat(bsp + (uint32_t)j * (uint32_t)sizeof(S), s);
                     Real mx, my, ca, cb, cc, al;
                     fields(s, mx, my, ca, cb, cc, al);
                     const Real dx = fx - mx;
                     const Real dy = fy - my;
                     const Real pw = half * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
                     if (pw > (Real)0 || pw < skip_lo) continue;
-                    const Real ai = al * splat_exp(pw, s_tab);
+                    const Real ai = al * splat_exp_s(pw, eops);
                     if (ai < floor_a) continue;
                     Real r, g, b;
                     colours(s, r, g, b);
@@ -282,7 +355,7 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
     if (i >= m) return;
     float ex, ey;
     cull_extents((double)conics[3 * i], (double)conics[3 * i + 1], (double)conics[3 * i + 2],
-                 sizeof(Real) == 4 ? 0x1p-23 : 0x1p-52, ex, ey);
+                 sizeof(Real) == 4 ? 0x1p-23 : 0x1p-52, ex, ey, (double)alphas[i]);
     if constexpr (sizeof(Real) == 4) {
         PayloadF32 p;
         p.a = make_float4(means2d[2 * i], means2d[2 * i + 1], conics[3 * i], conics[3 * i + 1]);

@@ -388,7 +388,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
         const long long m = m_base + lm;
         if (kF64) {
             float ex, ey;
-            cull_extents(o.ca, o.cb, o.cc, 0x1p-52, ex, ey);
+            cull_extents(o.ca, o.cb, o.cc, 0x1p-52, ex, ey, o.alpha);
             PayloadF64 p;
             p.a = make_double2(o.u, o.v);
             p.b = make_double2(o.ca, o.cb);
@@ -400,10 +400,11 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
         } else {
             const float fa = (float)o.ca, fb = (float)o.cb, fc = (float)o.cc;
             float ex, ey;
-            cull_extents_f32(fa, fb, fc, ex, ey);
+            const float fal = (float)o.alpha;
+            cull_extents_f32(fa, fb, fc, ex, ey, fal);
             PayloadF32 p;
             p.a = make_float4((float)o.u, (float)o.v, fa, fb);
-            p.b = make_float4(fc, (float)o.alpha, (float)o.r, (float)o.g);
+            p.b = make_float4(fc, fal, (float)o.r, (float)o.g);
             p.c = make_float4((float)o.b, ex, ey, 0.f);
             reinterpret_cast<PayloadF32 *>(ws.payload)[m] = p;
         }
