@@ -181,9 +181,13 @@ int g6r_profiler_read(g6r_profiler *prof, double *stage_ms, int32_t *views);
  * batches of `batch` views (1..8): every stage kernel processes a whole batch
  * per launch (grid = work x views), so one view's long tile runs overlap the
  * other views' work and the projection shares the record stream through L2.
- * The workspace must hold batch x g6r_workspace_bytes(...).  final_t /
- * last_contrib may be NULL in these frames.  prof may be NULL; it records one
- * slot per batch. */
+ * The workspace must hold batch x g6r_workspace_bytes(...).  When it holds
+ * twice that, there is more than one batch and prof is NULL, consecutive
+ * batches alternate between the two halves on two internal streams forked from
+ * and joined back into `stream` (a batch's projection and sort overlap the
+ * previous batch's compositing); the call stays asynchronous and ordered on
+ * `stream`.  final_t / last_contrib may be NULL in these frames.  prof may be
+ * NULL; it records one slot per batch (and keeps the batches on one stream). */
 int g6r_render_views(const g6r_scene *scene, uint32_t group_mask,
                      const g6r_camera *cams /* host array */, int32_t count,
                      const g6r_config *cfg, void *workspace, size_t workspace_bytes,

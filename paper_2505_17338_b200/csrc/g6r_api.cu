@@ -310,6 +310,24 @@ int g6r_render(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *ca
                         frame, splats, (cudaStream_t)stream, nullptr);
 }
 
+// Two internal streams per device for pipelining consecutive batches: a
+// batch's latency-bound projection and sort overlap the previous batch's
+// issue-bound compositing.
+static cudaStream_t g_lane[64][2];
+static std::mutex g_lane_mu;
+
+static int lane_streams(cudaStream_t *out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 1;
+    std::lock_guard<std::mutex> lock(g_lane_mu);
+    for (int k = 0; k < 2; ++k) {
+        if (!g_lane[dev][k] && cudaStreamCreateWithFlags(&g_lane[dev][k], cudaStreamNonBlocking) != cudaSuccess)
+            return 1;
+        out[k] = g_lane[dev][k];
+    }
+    return 0;
+}
+
 int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cams,
                      int32_t count, const g6r_config *cfg, void *workspace,
                      size_t workspace_bytes, int64_t entry_capacity, const g6r_frame *frames,
@@ -317,14 +335,48 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
     if (count < 0 || (count > 0 && (!cams || !frames))) return fail(G6R_EINVAL, "bad view list");
     if (count == 0) return G6R_OK;
     if (int rc = check_config(cfg)) return rc;
+    if (!scene) return fail(G6R_EINVAL, "scene is NULL");
     const int nb = batch < 1 ? 1 : (batch > kMaxBatch ? kMaxBatch : batch);
-    for (int32_t k = 0; k < count; k += nb) {
-        const int nv = count - k < nb ? count - k : nb;
-        const int rc = render_batch(scene, group_mask, &cams[k], nv, cfg, workspace, workspace_bytes,
-                                    entry_capacity, &frames[k], nullptr, (cudaStream_t)stream, prof);
-        if (rc) return rc;
+    const cudaStream_t st = (cudaStream_t)stream;
+    // Pipelined when the workspace holds two batches, there are at least two
+    // batches, and no profiler is attached (stage timings need one lane).
+    size_t per_batch = 0;
+    if (cams[0].width > 0 && cams[0].height > 0 && cfg->tile_size > 0) {
+        const int64_t tx = (cams[0].width + cfg->tile_size - 1) / cfg->tile_size;
+        const int64_t ty = (cams[0].height + cfg->tile_size - 1) / cfg->tile_size;
+        per_batch = layout(scene->n, tx * ty, entry_capacity, cfg->precision).total * (size_t)nb;
     }
-    return G6R_OK;
+    const bool piped = !prof && count > nb && per_batch && workspace_bytes >= 2 * per_batch;
+    if (!piped) {
+        for (int32_t k = 0; k < count; k += nb) {
+            const int nv = count - k < nb ? count - k : nb;
+            const int rc = render_batch(scene, group_mask, &cams[k], nv, cfg, workspace,
+                                        workspace_bytes, entry_capacity, &frames[k], nullptr, st, prof);
+            if (rc) return rc;
+        }
+        return G6R_OK;
+    }
+    cudaStream_t lane[2];
+    if (lane_streams(lane)) return cuda_check("lane streams");
+    cudaEvent_t fork, join[2];
+    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return cuda_check("event");
+    cudaEventRecord(fork, st);
+    for (int l = 0; l < 2; ++l) cudaStreamWaitEvent(lane[l], fork, 0);
+    int rc = G6R_OK;
+    for (int32_t k = 0, i = 0; k < count && !rc; k += nb, ++i) {
+        const int nv = count - k < nb ? count - k : nb;
+        char *half = static_cast<char *>(workspace) + (size_t)(i & 1) * per_batch;
+        rc = render_batch(scene, group_mask, &cams[k], nv, cfg, half, per_batch, entry_capacity,
+                          &frames[k], nullptr, lane[i & 1], nullptr);
+    }
+    for (int l = 0; l < 2; ++l) {   // join (also on error, so the caller's stream stays ordered)
+        cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
+        cudaEventRecord(join[l], lane[l]);
+        cudaStreamWaitEvent(st, join[l], 0);
+        cudaEventDestroy(join[l]);
+    }
+    cudaEventDestroy(fork);
+    return rc;
 }
 
 g6r_profiler *g6r_profiler_create(int32_t max_batches) {

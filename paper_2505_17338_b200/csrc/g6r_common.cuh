@@ -15,8 +15,9 @@ namespace g6r {
 
 constexpr int kBlock = 256;          // threads per CTA for streaming kernels
 constexpr int kMaxPasses = 8;        // radix passes (8-bit digits over <= 64-bit keys)
-constexpr int kSortItems = 16;       // keys per thread in a onesweep tile
-constexpr int kSortTile = kBlock * kSortItems;   // 4096 keys per tile
+constexpr int kSortItems = 8;        // keys per thread in a onesweep tile
+constexpr int kSortThreads = 256;    // threads per onesweep CTA
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per tile
 constexpr double kMinAlpha = 1.0 / 255.0;        // raster.py:47
 
 constexpr int kRadixBits = 9;                    // LSD digit width
@@ -204,6 +205,16 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 }
 __device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// GPU-scope relaxed accesses for look-back status words (volatile compiles to
+// system-scope strong accesses, which the look-back does not need).
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned *p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_volatile_u32(const unsigned *p) {
     unsigned v;

@@ -16,15 +16,17 @@
 // device per view; surplus work exits at once and consumers read which
 // ping-pong buffer holds the result (sorted_buffer()).
 //
-// Each pass is reduce-then-scan over 4096-key tiles, with no inter-CTA waiting
-// (grid y = view):
-//   upsweep    per-tile digit counts (warp match-any aggregated smem atomics)
-//              + global digit totals;
-//   colscan    exclusive scan of every digit column across tiles;
-//   downsweep  re-rank each tile (stable: warp-striped items, warps in order),
-//              scatter to global digit offset + column prefix + local rank.
-// (A decoupled look-back version was latency-bound: its inclusive-prefix
-// frontier advances one probe width per L2 round trip, ~30 us per pass.)
+// Each pass is ONE "onesweep" kernel (grid y = view): a CTA claims the next
+// 2048-key tile of its view through an atomic ticket, ranks the tile's keys
+// (stable: warp-striped items, warps in order), publishes the tile's digit
+// counts, and finds its global digit offsets by decoupled look-back over the
+// earlier tiles' status words (2-bit flag | 30-bit count in one 32-bit word,
+// so a single store publishes both and no fence is needed).  The look-back
+// reads 8 predecessors per round trip.  One histogram launch before the passes
+// computes every pass's digit totals (LSD digit counts do not depend on the
+// order) and zeroes the status words.  With a batch of views per launch the
+// views' look-back chains run side by side, so the pass is bandwidth-bound
+// (24 B read+written per key) rather than bound by one chain's latency.
 #include <algorithm>
 
 #include "g6r_common.cuh"
@@ -84,93 +86,100 @@ __device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int p
 
 __device__ __forceinline__ int pass_src(int pass) { return pass & 1; }
 
+constexpr unsigned kAgg = 1u << 30, kInc = 2u << 30, kCntMask = (1u << 30) - 1;
+constexpr int kProbe = 4;   // look-back predecessors read per round trip
+
+// Digit totals of every pass in one read of the keys; zero the status words.
+// Each warp counts into its own shared histogram with plain shared atomics.
+constexpr int kHistWarps = 4;   // warp histograms per CTA (warps 2w, 2w+1 share one)
 __global__ void __launch_bounds__(kBlock)
-k_upsweep(const __grid_constant__ Batch b, int tbits, int pass) {
-    __shared__ unsigned h[kBins];
+k_sort_hist(const __grid_constant__ Batch b, int tbits) {
+    __shared__ unsigned h[kHistWarps][4][kBins];   // up to 4 passes counted in smem
     const int v = blockIdx.y;
     PassCtx c;
-    const bool run = pass_ctx(b, v, tbits, pass, c);
+    const bool run = pass_ctx(b, v, tbits, 0, c);
     const Workspace &ws = b.ws[v];
-    if (pass == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c.e <= ws.entry_capacity)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && c.e <= ws.entry_capacity)
         ws.internal[kSortPasses] = run ? c.passes : 0;
     if (!run) return;
-    const unsigned long long *__restrict__ keys = ws.keys[pass_src(pass)];
-    unsigned *counts = ws.sort_counts + (int64_t)pass * ws.sort_tiles_cap * kBins;
-    unsigned *totals = ws.hist + pass * kBins;
-    const int shift = kRadixBits * pass;
-    const int lane = threadIdx.x & 31;
-    for (int64_t tile = blockIdx.x; tile < c.ntiles; tile += gridDim.x) {
-        for (int k = threadIdx.x; k < kBins; k += kBlock) h[k] = 0u;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+    {   // zero this view's status words for the passes that run (16-byte stores)
+        uint4 *st = reinterpret_cast<uint4 *>(ws.sort_counts);
+        const int64_t per = ws.sort_tiles_cap * kBins / 4, used = c.ntiles * kBins / 4;
+        for (int p = 0; p < c.passes; ++p)
+            for (int64_t k = gtid; k < used; k += gsz) st[p * per + k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    const unsigned long long *__restrict__ keys = ws.keys[0];
+    const int hw = (threadIdx.x >> 5) % kHistWarps;
+    for (int p0 = 0; p0 < c.passes; p0 += 4) {   // 4 passes per read of the keys
+        const int np = c.passes - p0 < 4 ? c.passes - p0 : 4;
+        for (int k = threadIdx.x; k < kHistWarps * 4 * kBins; k += kBlock) (&h[0][0][0])[k] = 0u;
         __syncthreads();
-        const int64_t base = tile * kSortTile;
-        unsigned long long key[kSortItems];
-#pragma unroll
-        for (int k = 0; k < kSortItems; ++k) {   // all loads in flight first
-            const int64_t idx = base + k * kBlock + threadIdx.x;
-            key[k] = idx < c.e ? keys[idx] : 0ull;
-        }
-#pragma unroll
-        for (int k = 0; k < kSortItems; ++k) {
-            const int64_t idx = base + k * kBlock + threadIdx.x;
-            const unsigned d = idx < c.e ? digit_of(key[k], c.dmin, c.dbits, shift) : (unsigned)kBins;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (d < (unsigned)kBins && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
+        for (int64_t i = gtid; i < c.e; i += gsz) {
+            const unsigned long long key = keys[i];
+            for (int p = 0; p < np; ++p)
+                atomicAdd(&h[hw][p][digit_of(key, c.dmin, c.dbits, kRadixBits * (p0 + p))], 1u);
         }
         __syncthreads();
-        for (int d = threadIdx.x; d < kBins; d += kBlock) {
-            const unsigned cnt = h[d];
-            counts[tile * kBins + d] = cnt;
-            if (cnt) atomicAdd(&totals[d], cnt);
+        for (int k = threadIdx.x; k < np * kBins; k += kBlock) {
+            unsigned cnt = 0;
+#pragma unroll
+            for (int w = 0; w < kHistWarps; ++w) cnt += (&h[w][0][0])[k];
+            if (cnt) atomicAdd(&ws.hist[p0 * kBins + k], cnt);
         }
         __syncthreads();
     }
 }
 
-// Exclusive scan of each digit column across tiles.  CTA x owns 32 digit
-// columns (lane = digit); its 8 warps each sum a contiguous chunk of tiles,
-// the chunk sums are scanned in smem, then each warp rewrites its chunk.
-__global__ void __launch_bounds__(kBlock)
-k_colscan(const __grid_constant__ Batch b, int tbits, int pass) {
-    __shared__ unsigned s_sum[kWarps][32];
-    const int v = blockIdx.y;
-    PassCtx c;
-    if (!pass_ctx(b, v, tbits, pass, c)) return;
-    const Workspace &ws = b.ws[v];
-    unsigned *counts = ws.sort_counts + (int64_t)pass * ws.sort_tiles_cap * kBins;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int d = blockIdx.x * 32 + lane;
-    const int64_t per = ceil_div(c.ntiles, kWarps);
-    const int64_t t0 = warp * per, t1 = std::min<int64_t>(c.ntiles, t0 + per);
-    constexpr int U = 8;   // independent loads in flight per lane
-    unsigned s = 0;
-    for (int64_t t = t0; t < t1; t += U) {
-        unsigned x[U];
+// Exclusive count of digit d over tiles [0, tile): decoupled look-back.  The
+// immediate predecessor is read alone first (usually already inclusive); then
+// kProbe predecessors per round trip.
+__device__ __forceinline__ unsigned look_back(const unsigned *status, int64_t tile, int d) {
+    unsigned excl = 0;
+    int64_t j = tile - 1;
+    unsigned w0 = ld_relaxed_u32(status + j * kBins + d);
+    while (!(w0 & ~kCntMask)) w0 = ld_relaxed_u32(status + j * kBins + d);
+    excl = w0 & kCntMask;
+    if ((w0 & ~kCntMask) == kInc || j == 0) return excl;
+    --j;
+    while (true) {
+        unsigned w[kProbe];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = t + u < t1 ? counts[(t + u) * kBins + d] : 0u;
+        for (int q = 0; q < kProbe; ++q)
+            w[q] = j - q >= 0 ? ld_relaxed_u32(status + (j - q) * kBins + d) : kInc;
+        int adv = kProbe;
+        bool stop = false;
 #pragma unroll
-        for (int u = 0; u < U; ++u) s += x[u];
-    }
-    s_sum[warp][lane] = s;
-    __syncthreads();
-    unsigned run = 0;
-    for (int w = 0; w < warp; ++w) run += s_sum[w][lane];
-    for (int64_t t = t0; t < t1; t += U) {
-        unsigned x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = t + u < t1 ? counts[(t + u) * kBins + d] : 0u;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (t + u < t1) counts[(t + u) * kBins + d] = run;
-            run += x[u];
+        for (int q = 0; q < kProbe; ++q) {
+            if (stop) continue;
+            const unsigned fl = w[q] & ~kCntMask;
+            if (!fl) {   // not yet published: re-poll from here
+                adv = q;
+                stop = true;
+                continue;
+            }
+            excl += w[q] & kCntMask;
+            if (fl == kInc) return excl;
         }
+        j -= adv;
     }
 }
 
-__global__ void __launch_bounds__(kBlock)
-k_downsweep(const __grid_constant__ Batch b, int tbits, int pass) {
+constexpr int kOsWarps = kSortThreads / 32;
+
+// One CTA of 256 threads per 2048-key tile (64 registers, so 4 CTAs share an
+// SM and one CTA's look-back wait overlaps the others' loads and ranking):
+// 8 warps rank their 256 keys each into per-warp 16-bit digit counters; each
+// thread then owns two digits for the prefix over warps, the status publish
+// and the look-back.
+__global__ void __launch_bounds__(kSortThreads, 4)
+k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
     __shared__ unsigned s_goff[kBins];
-    __shared__ unsigned s_wh[kWarps][kBins];
-    __shared__ unsigned s_scan[kWarps];
+    __shared__ unsigned short s_wh[kOsWarps][kBins];
+    __shared__ unsigned s_base[kBins];
+    __shared__ unsigned s_scan[kOsWarps];
+    __shared__ long long s_tile;
     const int v = blockIdx.y;
     PassCtx c;
     if (!pass_ctx(b, v, tbits, pass, c)) return;
@@ -180,31 +189,41 @@ k_downsweep(const __grid_constant__ Batch b, int tbits, int pass) {
     const unsigned *__restrict__ vin = ws.vals[src];
     unsigned long long *__restrict__ kout = ws.keys[src ^ 1];
     unsigned *__restrict__ vout = ws.vals[src ^ 1];
-    const unsigned *counts = ws.sort_counts + (int64_t)pass * ws.sort_tiles_cap * kBins;
+    unsigned *status = ws.sort_counts + (int64_t)pass * ws.sort_tiles_cap * kBins;
     const unsigned *totals = ws.hist + pass * kBins;
+    unsigned long long *ticket = reinterpret_cast<unsigned long long *>(&ws.internal[kTicketSortBase + pass]);
     const int shift = kRadixBits * pass;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    {   // global exclusive digit offsets: thread t owns digits 2t, 2t+1
-        const unsigned c0 = totals[2 * tid], c1 = totals[2 * tid + 1];
-        const unsigned cc = c0 + c1;
+    constexpr int kOwn = kBins / kSortThreads;   // digits per thread
+    {   // global exclusive digit offsets: thread t owns digits kOwn*t ..
+        unsigned cnt[kOwn], cc = 0;
+#pragma unroll
+        for (int q = 0; q < kOwn; ++q) cc += (cnt[q] = totals[kOwn * tid + q]);
         const unsigned inc = warp_inclusive_scan(cc);
         if (lane == 31) s_scan[warp] = inc;
         __syncthreads();
         unsigned pre = 0;
         for (int w = 0; w < warp; ++w) pre += s_scan[w];
-        s_goff[2 * tid] = pre + inc - cc;
-        s_goff[2 * tid + 1] = pre + inc - cc + c0;
+        unsigned run = pre + inc - cc;
+#pragma unroll
+        for (int q = 0; q < kOwn; ++q) {
+            s_goff[kOwn * tid + q] = run;
+            run += cnt[q];
+        }
     }
     const unsigned lanemask_lt = (1u << lane) - 1u;
-    for (int64_t tile = blockIdx.x; tile < c.ntiles; tile += gridDim.x) {
-        for (int k = tid; k < kWarps * kBins; k += kBlock) (&s_wh[0][0])[k] = 0u;
+    while (true) {
+        if (tid == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+        for (int k = tid; k < kOsWarps * kBins / 2; k += kSortThreads)
+            reinterpret_cast<unsigned *>(&s_wh[0][0])[k] = 0u;
         __syncthreads();
-        // warp w owns the contiguous items [w*512, w*512+512) of the tile, striped
+        const int64_t tile = s_tile;
+        if (tile >= c.ntiles) break;
+        // warp w owns the contiguous items [w*256, w*256+256) of the tile, striped
         const int64_t base = tile * kSortTile + (int64_t)warp * (32 * kSortItems);
         unsigned long long key[kSortItems];
         unsigned val[kSortItems];
-        unsigned dig[kSortItems];
-        unsigned rank[kSortItems];
+        unsigned dr[kSortItems];   // digit << 16 | rank within the warp
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             const int64_t idx = base + k * 32 + lane;
@@ -215,40 +234,49 @@ k_downsweep(const __grid_constant__ Batch b, int tbits, int pass) {
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             const int64_t idx = base + k * 32 + lane;
-            dig[k] = idx < c.e ? digit_of(key[k], c.dmin, c.dbits, shift) : (unsigned)kBins;
-        }
-#pragma unroll
-        for (int k = 0; k < kSortItems; ++k) {
-            const unsigned d = dig[k];
-            rank[k] = 0xffffffffu;
+            const unsigned d = idx < c.e ? digit_of(key[k], c.dmin, c.dbits, shift) : (unsigned)kBins;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
             if (d < (unsigned)kBins && lane == leader) {
                 old = s_wh[warp][d];
-                s_wh[warp][d] = old + (unsigned)__popc(peers);
+                s_wh[warp][d] = (unsigned short)(old + (unsigned)__popc(peers));
             }
             old = __shfl_sync(0xffffffffu, old, leader);
-            if (d < (unsigned)kBins) rank[k] = old + (unsigned)__popc(peers & lanemask_lt);
+            dr[k] = d << 16 | (old + (unsigned)__popc(peers & lanemask_lt));
             __syncwarp();
         }
         __syncthreads();
+        unsigned tot[kOwn];
 #pragma unroll
-        for (int q = 0; q < kDigitsPerThread; ++q) {   // tile base + exclusive prefix over warps
-            const int d = tid + q * kBlock;
-            unsigned run = s_goff[d] + counts[tile * kBins + d];
+        for (int q = 0; q < kOwn; ++q) {   // exclusive prefix over warps, publish
+            const int d = tid + q * kSortThreads;
+            unsigned run = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
+            for (int w = 0; w < kOsWarps; ++w) {
                 const unsigned cnt = s_wh[w][d];
-                s_wh[w][d] = run;
+                s_wh[w][d] = (unsigned short)run;
                 run += cnt;
             }
+            tot[q] = run;
+            st_relaxed_u32(status + tile * kBins + d, (tile == 0 ? kInc : kAgg) | run);
+        }
+#pragma unroll
+        for (int q = 0; q < kOwn; ++q) {   // look back
+            const int d = tid + q * kSortThreads;
+            unsigned excl = 0;
+            if (tile > 0) {
+                excl = look_back(status, tile, d);
+                st_relaxed_u32(status + tile * kBins + d, kInc | (excl + tot[q]));
+            }
+            s_base[d] = s_goff[d] + excl;
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
-            if (dig[k] >= (unsigned)kBins) continue;
-            const unsigned pos = s_wh[warp][dig[k]] + rank[k];
+            const unsigned d = dr[k] >> 16;
+            if (d >= (unsigned)kBins) continue;
+            const unsigned pos = s_base[d] + s_wh[warp][d] + (dr[k] & 0xffffu);
             kout[pos] = key[k];
             vout[pos] = val[k];
         }
@@ -308,16 +336,15 @@ int launch_sort(const Batch &b, cudaStream_t st) {
     const int max_passes = sort_passes((int)n_tiles);
     const int sms = num_sms();
     const int64_t tiles_cap = b.ws[0].sort_tiles_cap;
-    // per view: one CTA per 4096-key tile of the capacity (idle ones exit), grid-stride beyond
-    const unsigned gx = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(tiles_cap, std::max<int64_t>(sms * 8 / b.nviews, 1)));
+    const unsigned hx = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(b.ws[0].entry_capacity, kBlock), std::max(sms * 4 / b.nviews, 1)));
+    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, tbits);
+    trace_mark("sort_hist", st);
+    const unsigned ox = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(tiles_cap, std::max<int64_t>(sms * 4 / b.nviews, 1)));
     for (int p = 0; p < max_passes; ++p) {
-        k_upsweep<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b, tbits, p);
-        trace_mark("upsweep", st);
-        k_colscan<<<dim3(kBins / 32, b.nviews), kBlock, 0, st>>>(b, tbits, p);
-        trace_mark("colscan", st);
-        k_downsweep<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b, tbits, p);
-        trace_mark("downsweep", st);
+        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, tbits, p);
+        trace_mark("onesweep", st);
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }

@@ -512,7 +512,7 @@ DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
                  capacity: int | None = None, out=None, profiler=None,
                  concurrency: int = DEFAULT_CONCURRENCY, rgba8=None, background=(0.0, 0.0, 0.0),
-                 image: bool = True):
+                 image: bool = True, pipeline: bool = True):
     """Render ``cameras`` (same size) with up to ``concurrency`` views in flight.
 
     Returns ``(images, counters)``: ``images`` (V,H,W,4) on the device,
@@ -546,7 +546,9 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     slots = max(1, min(int(concurrency), 8, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
-    ws = torch.empty(max(per * slots, 256), dtype=torch.uint8, device=dev)
+    # two batches' worth pipelines consecutive batches on two streams
+    lanes = 2 if (V > slots and profiler is None and pipeline) else 1
+    ws = torch.empty(max(per * slots * lanes, 256), dtype=torch.uint8, device=dev)
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
     bg = (ctypes.c_double * 3)(*[float(c) for c in background])
     frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr() if images is not None else 0, 0, 0,
@@ -555,11 +557,23 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
                                for v in range(V)])
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
-                                          _ptr(ws), per * slots, cap, frames, slots,
+                                          _ptr(ws), per * slots * lanes, cap, frames, slots,
                                           profiler.handle if profiler is not None else None,
                                           _stream_handle()))
     counters._g6r_keepalive = ws
     return images, counters
+
+
+_LANES = {}
+
+
+def _render_lanes(dev):
+    """Two render streams and a copy stream per device, reused across calls."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    lanes = _LANES.get(key)
+    if lanes is None:
+        lanes = _LANES[key] = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
+    return lanes
 
 
 def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
@@ -567,10 +581,12 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     """Render many views to host memory: (V, H, W, 4) like stacking
     ``render(scene, cam)`` over ``cameras``.
 
-    Views are rendered ``batch`` per launch on the current stream; each chunk's
-    images are copied device->host into pinned memory on a side stream while
-    the next chunk renders.  One synchronisation at the end; views that
-    overflowed the entry capacity are re-rendered individually."""
+    Views are rendered ``batch`` per launch, consecutive chunks alternating
+    between two render streams (one chunk's projection and sort overlap the
+    other's compositing); each chunk's images are copied device->host into
+    pinned memory on a side stream while later chunks render.  One
+    synchronisation at the end; views that overflowed the entry capacity are
+    re-rendered individually."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cams = list(cameras)
@@ -585,22 +601,28 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     # recycles the block once the array is released): no extra host copy
     host = torch.empty((V, H, W, 4), dtype=dt, pin_memory=True)
     main = torch.cuda.current_stream()
-    copy = torch.cuda.Stream(device=dev)
+    lanes = _render_lanes(dev)
+    copy = lanes[2]
+    for ln in lanes:
+        ln.wait_stream(main)
     counters = []
     chunk = max(1, min(int(batch), 8))
-    for k in range(0, V, chunk):
+    for i, k in enumerate(range(0, V, chunk)):
         sl = slice(k, min(V, k + chunk))
-        _, cnt = render_views(scene, cams[sl], group_mask, config, out=images[sl],
-                              concurrency=chunk)
+        lane = lanes[i & 1]
+        with torch.cuda.stream(lane):
+            _, cnt = render_views(scene, cams[sl], group_mask, config, out=images[sl],
+                                  concurrency=chunk)
         counters.append(cnt)
         ev = torch.cuda.Event()
-        ev.record(main)
+        ev.record(lane)
         copy.wait_event(ev)
         with torch.cuda.stream(copy):
             host[sl].copy_(images[sl], non_blocking=True)
-            images[sl].record_stream(copy)
+    for ln in lanes:
+        main.wait_stream(ln)
     copy.synchronize()
-    cnt = torch.cat(counters).cpu().numpy()
+    cnt = torch.cat([c.to(dev) for c in counters]).cpu().numpy()
     out = host.numpy()
     for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
         fr, _ = _render_checked(prep, bits, cams[v], config, False)
