@@ -268,16 +268,18 @@ struct EmitSmem {
     int x0[kBlock], y0[kBlock], wx[kBlock];
     float rwx[kBlock];  // 1 / wx, for a division-free row/column split
     unsigned db[kBlock];   // f32 depth bits
+    unsigned idx[kBlock];  // entry value: compacted splat index or scene row
 };
 
 __device__ __forceinline__ void stage_rect(EmitSmem &es, int l, int eoff, int x0, int y0, int wx,
-                                           unsigned db) {
+                                           unsigned db, unsigned idx) {
     es.eoff[l] = eoff;
     es.x0[l] = x0;
     es.y0[l] = y0;
     es.wx[l] = wx;
     es.rwx[l] = 1.0f / (float)wx;
     es.db[l] = db;
+    es.idx[l] = idx;
 }
 
 // Cooperative duplication of this CTA's kept splats into (key, value) entries,
@@ -285,9 +287,8 @@ __device__ __forceinline__ void stage_rect(EmitSmem &es, int l, int eoff, int x0
 // np.repeat produces in raster.py:369-375).  Entry j of the CTA belongs to the
 // largest l with eoff[l] <= j (binary search); the row/column split uses a
 // float reciprocal corrected to the exact integer quotient.
-__device__ __forceinline__ void emit_entries(int nk, int ne, long long m_base, long long e_base,
-                                             const EmitSmem &es, int tiles_x,
-                                             unsigned long long *keys, unsigned *vals) {
+__device__ __forceinline__ void emit_entries(int nk, int ne, long long e_base, const EmitSmem &es,
+                                             int tiles_x, unsigned long long *keys, unsigned *vals) {
     for (int j = threadIdx.x; j < ne; j += blockDim.x) {
         int lo = 0, hi = nk - 1;
         while (lo < hi) {
@@ -304,7 +305,7 @@ __device__ __forceinline__ void emit_entries(int nk, int ne, long long m_base, l
         const int tx = es.x0[lo] + (loc - q * w);
         const unsigned long long tile = (unsigned long long)ty * (unsigned)tiles_x + (unsigned)tx;
         keys[e_base + j] = (tile << 32) | es.db[lo];
-        vals[e_base + j] = (unsigned)(m_base + lo);
+        vals[e_base + j] = es.idx[lo];
     }
 }
 
@@ -322,7 +323,17 @@ __device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *
 // grid = (views, ceil(n / 256)): CTA (v, *) projects 256 Gaussians for view v.
 // The CTAs of the batch's views for one Gaussian block are adjacent in launch
 // order, so views 2..K read the block's records from L2.
-template <bool kF64>
+//
+// kOrdered: splats are compacted in scene order (the SplatBatch contract,
+// raster.py:157-170) through a decoupled look-back, and entries carry the
+// compacted index -- needed when SplatBatch outputs or per-splat rects are
+// requested (render_with_state, the backward pass).  Otherwise (the render
+// hot path) payloads stay at their scene row, entries carry the row, and a
+// CTA reserves its entry block with one atomic: no chain between CTAs.  The
+// entry array is then in CTA-completion order, so equal sort keys are put
+// back in row order after the sort (k_ranges), which is the reference's tie
+// rule (rows ascend with the compacted index).
+template <bool kF64, bool kOrdered>
 __global__ void __launch_bounds__(kBlock)
 k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_splat_out so,
           int write_entries, double sh_c0, double sh_c1) {
@@ -381,11 +392,18 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     depth_extrema(kept, db, s_dext);
     int lm, le, bm, be;
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
-    lookback2(tile, bm, be, ws, &s_pm, &s_pe);
+    if (kOrdered) {
+        lookback2(tile, bm, be, ws, &s_pm, &s_pe);
+    } else if (threadIdx.x == 0) {   // reserve this CTA's entry block; count its splats
+        s_pm = 0;
+        s_pe = (long long)atomicAdd((unsigned long long *)&counters[G6R_CNT_ENTRIES],
+                                    (unsigned long long)be);
+        if (bm) atomicAdd((unsigned long long *)&counters[G6R_CNT_DRAWN], (unsigned long long)bm);
+    }
     __syncthreads();
     const long long m_base = s_pm, e_base = s_pe;
     if (kept) {
-        const long long m = m_base + lm;
+        const long long m = kOrdered ? m_base + lm : i;
         if (kF64) {
             float ex, ey;
             cull_extents(o.ca, o.cb, o.cc, 0x1p-52, ex, ey, o.alpha);
@@ -408,6 +426,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             p.c = make_float4((float)o.b, ex, ey, 0.f);
             reinterpret_cast<PayloadF32 *>(ws.payload)[m] = p;
         }
+        if (kOrdered) {
         if (so.gids) so.gids[m] = i;
         if (so.means2d) {
             so.means2d[2 * m] = o.u;
@@ -429,8 +448,9 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             so.radii[2 * m] = o.rx;
             so.radii[2 * m + 1] = o.ry;
         }
-        stage_rect(es, lm, le, x0, y0, wx, db);
-        if (ws.splat_rect) ws.splat_rect[m] = make_int4((int)(e_base + le), x0, y0, wx);
+        }
+        stage_rect(es, lm, le, x0, y0, wx, db, (unsigned)m);
+        if (kOrdered && ws.splat_rect) ws.splat_rect[m] = make_int4((int)(e_base + le), x0, y0, wx);
     }
     __syncthreads();
     if (threadIdx.x < 6 && s_fate[threadIdx.x])
@@ -439,12 +459,12 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
     if (write_entries) {
         if (e_base + be <= ws.entry_capacity) {
-            emit_entries(bm, be, m_base, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
+            emit_entries(bm, be, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
         } else if (threadIdx.x == 0) {
             counters[G6R_CNT_OVERFLOW] = 1;
         }
     }
-    if (tile == gridDim.y - 1 && threadIdx.x == 0) {
+    if (kOrdered && tile == gridDim.y - 1 && threadIdx.x == 0) {
         counters[G6R_CNT_DRAWN] = m_base + bm;
         counters[G6R_CNT_ENTRIES] = e_base + be;
     }
@@ -478,12 +498,12 @@ k_duplicate(int64_t m, const double *__restrict__ means2d, const int32_t *__rest
     block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
     lookback2(tile, bm, be, ws, &s_pm, &s_pe);
     __syncthreads();
-    if (kept) stage_rect(es, lm, le, x0, y0, wx, db);
+    const long long m_base = s_pm, e_base = s_pe;
+    if (kept) stage_rect(es, lm, le, x0, y0, wx, db, (unsigned)(m_base + lm));
     __syncthreads();
     if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
-    const long long m_base = s_pm, e_base = s_pe;
     if (e_base + be <= ws.entry_capacity) {
-        emit_entries(bm, be, m_base, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
+        emit_entries(bm, be, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
     } else if (threadIdx.x == 0) {
         counters[G6R_CNT_OVERFLOW] = 1;
     }
@@ -548,10 +568,18 @@ int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
     if (splats) so = *splats;
     if (scene.n == 0 || b.nviews == 0) return G6R_OK;
     const dim3 grid((unsigned)b.nviews, (unsigned)ceil_div(scene.n, kBlock));
-    if (b.vp[0].precision)
-        k_project<true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    // compacted (ordered) only when SplatBatch-shaped outputs or rects are wanted
+    const bool ordered = !write_entries || so.gids || so.means2d || so.conics || so.colors ||
+                         so.alphas || so.depths || so.radii || so.stage || b.ws[0].splat_rect;
+    const bool f64 = b.vp[0].precision != 0;
+    if (f64 && ordered)
+        k_project<true, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    else if (f64)
+        k_project<true, false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    else if (ordered)
+        k_project<false, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else
-        k_project<false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+        k_project<false, false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     trace_mark("project", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }

@@ -284,7 +284,25 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
     }
 }
 
-// grid y = view: tile_starts from the boundaries of the sorted keys.
+// Ascending in-place sort of a run of equal-key values (shell sort: runs are
+// almost always 2-3 long; a degenerate axis-aligned view can make long ones).
+__device__ void sort_run(unsigned *v, int n) {
+    int gap = 1;
+    while (gap < n / 3) gap = 3 * gap + 1;
+    for (; gap > 0; gap /= 3)
+        for (int a = gap; a < n; ++a) {
+            const unsigned x = v[a];
+            int c = a;
+            while (c >= gap && v[c - gap] > x) {
+                v[c] = v[c - gap];
+                c -= gap;
+            }
+            v[c] = x;
+        }
+}
+
+// grid y = view: tile_starts from the boundaries of the sorted keys, and the
+// row-order fix-up of equal-key runs.
 __global__ void __launch_bounds__(kBlock)
 k_ranges(const __grid_constant__ Batch b) {
     const int v = blockIdx.y;
@@ -305,16 +323,26 @@ k_ranges(const __grid_constant__ Batch b) {
     }
     const int fb = sorted_buffer(ws.internal);
     const unsigned long long *keys = ws.keys[fb];
-    const unsigned *vals = ws.vals[fb];
+    unsigned *vals = ws.vals[fb];
     int32_t *entry_out = out.entry_splat;
     for (int64_t i = gtid; i <= e; i += gsz) {
-        const int64_t ti = i < e ? (int64_t)(keys[i] >> 32) : n_tiles;
-        const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> 32) : -1;
+        const unsigned long long ki = i < e ? keys[i] : ~0ull;
+        const int64_t ti = i < e ? (int64_t)(ki >> 32) : n_tiles;
+        const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
+        const int64_t tp = i > 0 ? (int64_t)(kp >> 32) : -1;
         for (int64_t t = tp + 1; t <= ti; ++t) {
             starts[t] = i;
             if (starts2) starts2[t] = i;
         }
-        if (i < e && entry_out) entry_out[i] = (int32_t)vals[i];
+        if (i >= e || (i > 0 && kp == ki)) continue;   // runs are handled by their first entry
+        // Equal keys (same tile, same f32 depth) must end in row order, the
+        // reference's stable tie rule: the chain-free projection emits CTA
+        // blocks in completion order, so sort each such run by value.
+        int64_t j = i + 1;
+        while (j < e && keys[j] == ki) ++j;
+        if (j - i > 1) sort_run(vals + i, (int)(j - i));
+        if (entry_out)
+            for (int64_t k = i; k < j; ++k) entry_out[k] = (int32_t)vals[k];
     }
 }
 
