@@ -27,6 +27,15 @@
  *   g6r_composite        raster.py:392-415 _composite / _kernels.pyx:36-105
  *   g6r_composite_backward _kernels.pyx:108-187
  *   g6r_render           raster.py:443-466 render_with_state / render
+ *   g6r_render_views     many views of one scene (batched, pipelined)
+ *   g6r_render_backward  diffrender.py:401-439 render_backward + :183-398 _backward_rows
+ *     (= g6r_backward_forward + g6r_backward_apply)
+ *   g6r_loss_grad        diffrender.py:117-138 _loss_parts, _ssim.py:123-201
+ *   g6r_adam_step        diffrender.py:481-509 adam_step
+ *   g6r_decode_records   sceneio.py:77-111 load_scene (record block)
+ *   g6r_decode_param_volume  priming.py:232-285 decode_param_volume
+ *   g6r_filter_rows      priming.py:362-374 filter_scene
+ *   g6r_frame.rgba8      metrics.py:21-25 composite_over + _png.py:21-32 to_rgba_u8
  */
 #ifndef G6R_H_
 #define G6R_H_
