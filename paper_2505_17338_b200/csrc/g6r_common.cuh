@@ -76,7 +76,8 @@ __host__ __device__ __forceinline__ double cull_q(double alpha) {
     const double floor = 1.0 / 255.0;   // <= the f32 compositor's (float)(1/255)
     const double amax = alpha * (1.0 + 1e-5);
     if (!(amax > floor)) return -1.0;
-    const double qa = 2.0 * log(amax / floor) + 1e-4;
+    // single-precision log with generous margins (an upper bound is all we need)
+    const double qa = 2.0 * (double)logf((float)(amax / floor)) * (1.0 + 1e-4) + 1e-3;
     return qa < 9.0 ? qa : 9.0;
 }
 

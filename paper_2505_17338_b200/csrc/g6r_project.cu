@@ -134,10 +134,19 @@ __device__ __forceinline__ void tile_rect(double u, double v, int32_t rx, int32_
                                           const ViewParams &vp, int &x0, int &y0, int &wx,
                                           int &hy) {
     const double ts = (double)vp.tile_size;
-    long long a = (long long)floor((u - (double)rx) / ts);
-    long long b = (long long)floor((u + (double)rx) / ts);
-    long long c = (long long)floor((v - (double)ry) / ts);
-    long long d = (long long)floor((v + (double)ry) / ts);
+    long long a, b, c, d;
+    if ((vp.tile_size & (vp.tile_size - 1)) == 0) {   // x / 2^k == x * 2^-k exactly
+        const double its = 1.0 / ts;
+        a = (long long)floor((u - (double)rx) * its);
+        b = (long long)floor((u + (double)rx) * its);
+        c = (long long)floor((v - (double)ry) * its);
+        d = (long long)floor((v + (double)ry) * its);
+    } else {
+        a = (long long)floor((u - (double)rx) / ts);
+        b = (long long)floor((u + (double)rx) / ts);
+        c = (long long)floor((v - (double)ry) / ts);
+        d = (long long)floor((v + (double)ry) / ts);
+    }
     const long long mx = vp.tiles_x - 1, my = vp.tiles_y - 1;
     a = a < 0 ? 0 : (a > mx ? mx : a);
     b = b < 0 ? 0 : (b > mx ? mx : b);
@@ -269,6 +278,7 @@ struct EmitSmem {
     float rwx[kBlock];  // 1 / wx, for a division-free row/column split
     unsigned db[kBlock];   // f32 depth bits
     unsigned idx[kBlock];  // entry value: compacted splat index or scene row
+    int cnt[kBlock];       // entries of the splat (hybrid emission list)
 };
 
 __device__ __forceinline__ void stage_rect(EmitSmem &es, int l, int eoff, int x0, int y0, int wx,
@@ -309,6 +319,8 @@ __device__ __forceinline__ void emit_entries(int nk, int ne, long long e_base, c
     }
 }
 
+constexpr int kDirectEntries = 8;   // splats with at most this many tiles emit their own entries
+
 // Reduce a CTA's drawn-splat depth bits into the view's extrema (for the radix
 // key compression in g6r_sort.cu).  Called by every thread.
 __device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *s_dext) {
@@ -343,6 +355,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     __shared__ unsigned s_fate[6];
     __shared__ EmitSmem es;
     __shared__ unsigned s_dext[2];   // block max of ~depth_bits and of depth_bits
+    __shared__ int s_nbig;
     const int v = blockIdx.x;
     const ViewParams &vp = b.vp[v];
     const Workspace &ws = b.ws[v];
@@ -350,6 +363,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long *)&ws.internal[kTicketProject], 1ull);
     if (threadIdx.x < 6) s_fate[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_nbig = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t n = scene.n;
@@ -449,20 +463,52 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             so.radii[2 * m + 1] = o.ry;
         }
         }
-        stage_rect(es, lm, le, x0, y0, wx, db, (unsigned)m);
         if (kOrdered && ws.splat_rect) ws.splat_rect[m] = make_int4((int)(e_base + le), x0, y0, wx);
+    }
+    // Duplication, hybrid: a splat with few tiles writes its own entries (row-
+    // major over its rect); larger ones are queued and emitted by the whole CTA.
+    const bool emit_ok = write_entries && e_base + be <= ws.entry_capacity;
+    if (kept && emit_ok) {
+        const long long m = kOrdered ? m_base + lm : i;
+        if (cnt <= kDirectEntries) {
+            unsigned long long *keys = ws.keys[0] + e_base + le;
+            unsigned *vals = ws.vals[0] + e_base + le;
+            int k = 0;
+            for (int yy = 0; yy < hy; ++yy)
+                for (int xx = 0; xx < wx; ++xx, ++k) {
+                    const unsigned long long t =
+                        (unsigned long long)(y0 + yy) * (unsigned)vp.tiles_x + (unsigned)(x0 + xx);
+                    keys[k] = (t << 32) | db;
+                    vals[k] = (unsigned)m;
+                }
+        } else {
+            const int q = atomicAdd(&s_nbig, 1);
+            stage_rect(es, q, le, x0, y0, wx, db, (unsigned)m);
+            es.cnt[q] = cnt;
+        }
     }
     __syncthreads();
     if (threadIdx.x < 6 && s_fate[threadIdx.x])
         atomicAdd((unsigned long long *)&counters[G6R_CNT_FATE + threadIdx.x],
                   (unsigned long long)s_fate[threadIdx.x]);
     if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
-    if (write_entries) {
-        if (e_base + be <= ws.entry_capacity) {
-            emit_entries(bm, be, e_base, es, vp.tiles_x, ws.keys[0], ws.vals[0]);
-        } else if (threadIdx.x == 0) {
-            counters[G6R_CNT_OVERFLOW] = 1;
+    if (emit_ok) {
+        const int nbig = s_nbig;
+        for (int q = 0; q < nbig; ++q) {   // queued large rects, all threads per rect
+            const int n_e = es.cnt[q], w = es.wx[q], base = es.eoff[q];
+            const float rw = es.rwx[q];
+            for (int k = threadIdx.x; k < n_e; k += blockDim.x) {
+                int r = (int)((float)k * rw);
+                if (r * w > k) --r;
+                else if ((r + 1) * w <= k) ++r;
+                const unsigned long long t = (unsigned long long)(es.y0[q] + r) * (unsigned)vp.tiles_x +
+                                             (unsigned)(es.x0[q] + (k - r * w));
+                ws.keys[0][e_base + base + k] = (t << 32) | es.db[q];
+                ws.vals[0][e_base + base + k] = es.idx[q];
+            }
         }
+    } else if (write_entries && threadIdx.x == 0) {
+        counters[G6R_CNT_OVERFLOW] = 1;
     }
     if (kOrdered && tile == gridDim.y - 1 && threadIdx.x == 0) {
         counters[G6R_CNT_DRAWN] = m_base + bm;
