@@ -112,14 +112,25 @@ k_sort_hist(const __grid_constant__ Batch b, int tbits) {
     }
     const unsigned long long *__restrict__ keys = ws.keys[0];
     const int hw = (threadIdx.x >> 5) % kHistWarps;
+    constexpr int kH = 8;   // keys in flight per thread
     for (int p0 = 0; p0 < c.passes; p0 += 4) {   // 4 passes per read of the keys
         const int np = c.passes - p0 < 4 ? c.passes - p0 : 4;
         for (int k = threadIdx.x; k < kHistWarps * 4 * kBins; k += kBlock) (&h[0][0][0])[k] = 0u;
         __syncthreads();
-        for (int64_t i = gtid; i < c.e; i += gsz) {
-            const unsigned long long key = keys[i];
-            for (int p = 0; p < np; ++p)
-                atomicAdd(&h[hw][p][digit_of(key, c.dmin, c.dbits, kRadixBits * (p0 + p))], 1u);
+        for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kH + threadIdx.x; i0 < c.e;
+             i0 += gsz * kH) {
+            unsigned long long key[kH];
+#pragma unroll
+            for (int q = 0; q < kH; ++q) {
+                const int64_t i = i0 + (int64_t)q * blockDim.x;
+                key[q] = i < c.e ? keys[i] : 0ull;
+            }
+#pragma unroll
+            for (int q = 0; q < kH; ++q) {
+                if (i0 + (int64_t)q * blockDim.x >= c.e) break;
+                for (int p = 0; p < np; ++p)
+                    atomicAdd(&h[hw][p][digit_of(key[q], c.dmin, c.dbits, kRadixBits * (p0 + p))], 1u);
+            }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < np * kBins; k += kBlock) {
@@ -325,24 +336,36 @@ k_ranges(const __grid_constant__ Batch b) {
     const unsigned long long *keys = ws.keys[fb];
     unsigned *vals = ws.vals[fb];
     int32_t *entry_out = out.entry_splat;
-    for (int64_t i = gtid; i <= e; i += gsz) {
-        const unsigned long long ki = i < e ? keys[i] : ~0ull;
-        const int64_t ti = i < e ? (int64_t)(ki >> 32) : n_tiles;
-        const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
-        const int64_t tp = i > 0 ? (int64_t)(kp >> 32) : -1;
-        for (int64_t t = tp + 1; t <= ti; ++t) {
-            starts[t] = i;
-            if (starts2) starts2[t] = i;
+    constexpr int kR = 4;   // consecutive entries per thread per step (loads in flight)
+    for (int64_t i0 = gtid * kR; i0 <= e; i0 += gsz * kR) {
+        unsigned long long k[kR + 2];   // keys[i0-1 .. i0+kR]
+#pragma unroll
+        for (int q = 0; q < kR + 2; ++q) {
+            const int64_t i = i0 - 1 + q;
+            k[q] = (i >= 0 && i < e) ? keys[i] : ~0ull;
         }
-        if (i >= e || (i > 0 && kp == ki)) continue;   // runs are handled by their first entry
-        // Equal keys (same tile, same f32 depth) must end in row order, the
-        // reference's stable tie rule: the chain-free projection emits CTA
-        // blocks in completion order, so sort each such run by value.
-        int64_t j = i + 1;
-        while (j < e && keys[j] == ki) ++j;
-        if (j - i > 1) sort_run(vals + i, (int)(j - i));
-        if (entry_out)
-            for (int64_t k = i; k < j; ++k) entry_out[k] = (int32_t)vals[k];
+#pragma unroll
+        for (int q = 1; q <= kR; ++q) {
+            const int64_t i = i0 - 1 + q;
+            if (i > e) break;
+            const unsigned long long ki = k[q], kp = k[q - 1];
+            const int64_t ti = i < e ? (int64_t)(ki >> 32) : n_tiles;
+            const int64_t tp = i > 0 ? (int64_t)(kp >> 32) : -1;
+            for (int64_t t = tp + 1; t <= ti; ++t) {
+                starts[t] = i;
+                if (starts2) starts2[t] = i;
+            }
+            if (i >= e || (i > 0 && kp == ki)) continue;   // runs are handled by their first entry
+            // Equal keys (same tile, same f32 depth) must end in row order, the
+            // reference's stable tie rule: the chain-free projection emits CTA
+            // blocks in completion order, so sort each such run by value.
+            int64_t j = i + 1;
+            if (k[q + 1] == ki)
+                while (j < e && keys[j] == ki) ++j;
+            if (j - i > 1) sort_run(vals + i, (int)(j - i));
+            if (entry_out)
+                for (int64_t m = i; m < j; ++m) entry_out[m] = (int32_t)vals[m];
+        }
     }
 }
 

@@ -11,9 +11,9 @@ _, cnt = raster.render_views(s, cams[:8], concurrency=8)
 torch.cuda.synchronize()
 prep.entry_hint = int(cnt[:, 1].max().item() * 1.5) + 65536
 for batch in (8, 1):
-    raster.render_views(s, cams, concurrency=batch); torch.cuda.synchronize()
+    raster.render_views(s, cams, concurrency=batch, pipeline=False); torch.cuda.synchronize()
     nat.load().g6r_trace_dump(b"/tmp/trace_warm.csv")
-    raster.render_views(s, cams, concurrency=batch); torch.cuda.synchronize()
+    raster.render_views(s, cams, concurrency=batch, pipeline=False); torch.cuda.synchronize()
     path = f"gpurun_out/trace_b{batch}.csv"
     nat.load().g6r_trace_dump(path.encode())
     agg = collections.defaultdict(list)
