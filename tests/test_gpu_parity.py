@@ -100,6 +100,36 @@ def test_golden_end_to_end(name):
                 st.stats.n_projection_culled, st.stats.n_viewport_culled) == tuple(stats[2:7])
 
 
+@pytest.mark.parametrize("name", CASES)
+def test_golden_hot_path(name):
+    """The throughput path (chain-free projection: entries in CTA-completion
+    order, equal keys put back in row order after the sort) gives the golden
+    f32 image bit for bit -- incl. `ties50`, whose equal depths make the tie
+    rule visible in the compositing order."""
+    z, scene, cam, tile, w_mode = load_case(name)
+    cfg = RenderConfig(precision="f32", w_mode=w_mode, tile_size=tile)
+    imgs, counters = raster.render_views(scene, [cam] * 3, config=cfg)
+    c = counters.cpu().numpy()
+    assert int(c[:, 8].sum()) == 0
+    assert tuple(c[0, :2]) == tuple(z["stats"][:2])
+    for k in range(3):
+        np.testing.assert_array_equal(imgs[k].cpu().numpy(), z["f32_image"])
+    np.testing.assert_array_equal(raster.render(scene, cam, config=cfg), z["f32_image"])
+
+
+def test_pipelined_batches_match_unpipelined():
+    """19 views = three batches on the two pipelined streams vs one stream."""
+    s = scenes.random_scene(np.random.default_rng(72), 20000)
+    cams = scenes.orbit_ring(s, count=19, size=128)
+    a, ca = raster.render_views(s, cams)
+    b, cb = raster.render_views(s, cams, pipeline=False)
+    import torch
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(ca, cb)
+    host = raster.render_batch(s, cams)
+    np.testing.assert_array_equal(host, a.cpu().numpy())
+
+
 # --- stage gates ------------------------------------------------------------------
 
 @pytest.mark.parametrize("seed,n,w_mode", [(21, 3000, "peak"), (22, 3000, "raw")])
