@@ -182,7 +182,7 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // warp's pixel block; warps then ballot over the batch and visit only splats
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
-template <typename Real, int kNB>
+template <typename Real, int kNB, int kSub = 1>
 __global__ void __launch_bounds__(kNB > 0 ? kNB : 1024)
 k_composite(const __grid_constant__ Batch bt, int sorted) {
     using S = typename Px<Real>::S;
@@ -209,10 +209,15 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     const ExpOperands eops = exp_operands(smem_addr(s_tab));
 
     const int ts = vp.tile_size;
-    const int tile = blockIdx.x;
+    // kSub > 1 (16x16 tiles only): the tile's rows are split over kSub CTAs,
+    // each walking the whole run for its band, so a band that saturates early
+    // frees its SM slot instead of idling at the other band's barriers
+    const int tile = kSub > 1 ? (int)(blockIdx.x / kSub) : (int)blockIdx.x;
+    const int band = kSub > 1 ? (int)(blockIdx.x % kSub) * (16 / kSub) : 0;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     int ox, oy;
     tile_pixel(ts, threadIdx.x, ox, oy);
+    oy += band;
     const int px = tx * ts + ox;
     const int py = ty * ts + oy;
     const bool inside = px < vp.iw && py < vp.ih;
@@ -225,7 +230,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         if (ts == 16) {
             x0 = (w & 1) * 8;
             x1 = x0 + 7;
-            y0 = (w >> 1) * 4;
+            y0 = (w >> 1) * 4 + band;
             y1 = y0 + 3;
         } else {
             const int t0 = w * 32, t1 = min(nb, t0 + 32) - 1;
@@ -464,6 +469,8 @@ int launch_pack_payload(int64_t m, int precision, const void *means2d, const voi
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
+constexpr int kCompositeSub = 2;   // CTAs per 16x16 tile (f32 path)
+
 int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
     const ViewParams &vp = b.vp[0];
@@ -486,7 +493,8 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
             k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
         if (vp.tile_size == 16)
-            k_composite<float, 256><<<grid, 256, 0, st>>>(b, srt);
+            k_composite<float, 256 / kCompositeSub, kCompositeSub>
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
         else
             k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
     }
