@@ -353,7 +353,7 @@ def run_b200(args):
         # radix pass (upper bound of 9-bit passes; surplus ones exit at once),
         # ranges, composite
         max_passes = (32 + max(1, math.ceil(math.log2(T))) + 8) // 9
-        batches = math.ceil(V / max(1, min(args.concurrency, 8)))
+        batches = math.ceil(V / max(1, min(args.concurrency, 16)))
         launches = batches * (5 + max_passes)
         line = {
             "metric": METRIC, "value": views_per_s, "unit": UNIT, "n_gpus": world,

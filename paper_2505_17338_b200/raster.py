@@ -507,6 +507,7 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
 
 
 DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
+MAX_BATCH = 16            # kMaxBatch in csrc/g6r_internal.h
 
 
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
@@ -543,7 +544,7 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         raise InvalidParameterError(f"rgba8 must be a contiguous ({V}, {H}, {W}, 4) uint8 tensor")
     counters = torch.empty((V, nat.NCOUNTERS), dtype=torch.int64, device=dev)
     cap = int(capacity or prep.entry_hint)
-    slots = max(1, min(int(concurrency), 8, V))
+    slots = max(1, min(int(concurrency), MAX_BATCH, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
     # two batches' worth pipelines consecutive batches on two streams
@@ -606,7 +607,7 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     for ln in lanes:
         ln.wait_stream(main)
     counters = []
-    chunk = max(1, min(int(batch), 8))
+    chunk = max(1, min(int(batch), MAX_BATCH))
     for i, k in enumerate(range(0, V, chunk)):
         sl = slice(k, min(V, k + chunk))
         lane = lanes[i & 1]
@@ -648,7 +649,7 @@ def render_frames_u8(scene, cameras, background=(0.0, 0.0, 0.0), group_mask=None
     H, W = int(cams[0].height), int(cams[0].width)
     dev = prep.device
     frames = torch.empty((V, H, W, 4), dtype=torch.uint8, device=dev)
-    chunk = max(1, min(int(batch), 8))
+    chunk = max(1, min(int(batch), MAX_BATCH))
     host = None if device_out else torch.empty((V, H, W, 4), dtype=torch.uint8, pin_memory=True)
     main = torch.cuda.current_stream()
     copy = torch.cuda.Stream(device=dev)
