@@ -404,3 +404,49 @@ def test_backward_matches_oracle(oracle):
     K.composite_backward(s.means2d, s.conics, s.colors, s.alphas, en.entry_splat, en.tile_starts,
                          en.tiles_x, 16, st.final_t, st.last_contrib, g, got)
     np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12)
+
+
+# --- edge cases of the reference's input domain ---------------------------------------
+
+@pytest.mark.parametrize("size", [(1, 1), (17, 13), (16, 16), (33, 7)])
+@pytest.mark.parametrize("tile", [16, 8, 32])
+def test_odd_image_and_tile_sizes_match_oracle(oracle, size, tile):
+    s = scenes.random_scene(np.random.default_rng(size[0] * 7 + tile), 600, box=6.0)
+    cam = scenes.orbit_camera(azimuth=0.4, elevation=0.1, distance=25.0, width=size[0],
+                              height=size[1])
+    for prec in ("f32", "f64"):
+        cfg = RenderConfig(precision=prec, tile_size=tile)
+        want = oracle.render_with_state(s, cam, None, prec, tile_size=tile)
+        got = raster.render(s, cam, config=cfg)
+        if prec == "f32":
+            np.testing.assert_array_equal(got, want.image)
+        else:
+            assert_image_close(got, want.image)
+        imgs, _ = raster.render_views(s, [cam, cam], config=cfg)
+        np.testing.assert_array_equal(imgs[1].cpu().numpy(), got)
+
+
+def test_empty_scene_and_nothing_visible():
+    from paper_2505_17338_b200.scene import Scene
+    empty = Scene(mu_p=np.zeros((0, 3)), mu_d=np.zeros((0, 3)), cov_raw=np.zeros((0, 21)),
+                  sh=np.zeros((0, 12)), opacity_raw=np.zeros(0), labels=np.zeros(0, np.uint8))
+    cam = scenes.orbit_camera(width=40, height=24)
+    assert not raster.render(empty, cam).any()
+    st = raster.render_with_state(empty, cam)
+    assert st.stats.n_drawn == 0 and len(st.entries.entry_splat) == 0
+    assert not raster.render_frames_u8(empty, [cam], (1.0, 0.0, 0.0))[0][:, :, 1].any()
+    # a scene entirely behind the camera
+    s = scenes.random_scene(np.random.default_rng(3), 200, box=2.0)
+    behind = scenes.orbit_camera(azimuth=0.0, distance=70.0, width=32, height=32,
+                                 target=(0.0, 0.0, -200.0))   # looks away from the scene
+    img = raster.render(s, behind)
+    assert not img.any()
+
+
+def test_f64_batched_views_match_single_renders():
+    s = scenes.random_scene(np.random.default_rng(81), 3000)
+    cams = scenes.orbit_ring(s, count=10, size=64)
+    cfg = RenderConfig(precision="f64")
+    imgs, _ = raster.render_views(s, cams, config=cfg)
+    for k, cam in enumerate(cams):
+        np.testing.assert_array_equal(imgs[k].cpu().numpy(), raster.render(s, cam, config=cfg))
