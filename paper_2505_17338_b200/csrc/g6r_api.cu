@@ -243,9 +243,9 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     prof_mark(prof, 1, st);
     // (Sorting the batch in L2-sized sub-batches was measured slower: the extra
     //  launches cost more than the HBM traffic they save.)
-    if (launch_sort(b, st)) return cuda_check("sort");
+    if (launch_sort(b, scene->n, st)) return cuda_check("sort");
     prof_mark(prof, 2, st);
-    if (launch_ranges(b, st)) return cuda_check("ranges");
+    if (launch_ranges(b, scene->n, st)) return cuda_check("ranges");
     prof_mark(prof, 3, st);
     if (launch_composite(b, true, st)) return cuda_check("composite");
     prof_mark(prof, 4, st);
@@ -524,8 +524,8 @@ int g6r_backward_forward(const g6r_scene *scene, uint32_t group_mask, const g6r_
     const Layout L = layout(scene->n, (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y, entry_capacity, 1);
     if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     if (launch_project(*scene, group_mask, b, &so, true, st)) return cuda_check("project");
-    if (launch_sort(b, st)) return cuda_check("sort");
-    if (launch_ranges(b, st)) return cuda_check("ranges");
+    if (launch_sort(b, scene->n, st)) return cuda_check("sort");
+    if (launch_ranges(b, scene->n, st)) return cuda_check("ranges");
     if (launch_composite(b, true, st)) return cuda_check("composite");
     return G6R_OK;
 }
@@ -752,8 +752,8 @@ int g6r_bin(int64_t m, const double *means2d, const int32_t *radii, const double
     cudaStream_t st = (cudaStream_t)stream;
     if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     if (launch_duplicate(m, means2d, radii, depths, b, st)) return cuda_check("duplicate");
-    if (launch_sort(b, st)) return cuda_check("sort");
-    if (launch_ranges(b, st)) return cuda_check("ranges");
+    if (launch_sort(b, m, st)) return cuda_check("sort");
+    if (launch_ranges(b, m, st)) return cuda_check("ranges");
     return G6R_OK;
 }
 

@@ -29,13 +29,14 @@ enum {
     kTicketSortBase = 1,   // 1..8: one per radix pass
     kDepthMinInv = 10,     // ~min f32 depth bits of the drawn splats (atomicMax of ~bits)
     kDepthMax = 11,        // max f32 depth bits
+    kValsBuffer = 9,       // which vals buffer holds the sorted entry values
     kSortPasses = 12,      // radix passes actually needed (decided on the device)
     kNumInternal = 16
 };
 
-// Which ping-pong buffer holds the sorted entries after the radix passes.
+// Which ping-pong buffer holds the sorted entry values after the radix passes.
 __device__ __forceinline__ int sorted_buffer(const long long *internal) {
-    return (int)(internal[kSortPasses] & 1);
+    return (int)(internal[kValsBuffer] & 1);
 }
 
 // Fold a CTA's depth-bit extrema (max of ~bits, max of bits) into the view's.

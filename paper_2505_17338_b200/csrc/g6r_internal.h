@@ -81,9 +81,10 @@ int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
 int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, const double *depths,
                      const Batch &b, cudaStream_t st);
 // radix sort of every view's ws.keys[0]/vals[0] (E read from its counters)
-int launch_sort(const Batch &b, cudaStream_t st);
+// max_val: largest entry value (splat index) the views can carry
+int launch_sort(const Batch &b, int64_t max_val, cudaStream_t st);
 // per-tile ranges into ws.tile_starts (+ optional copies of starts / entry_splat)
-int launch_ranges(const Batch &b, cudaStream_t st);
+int launch_ranges(const Batch &b, int64_t max_val, cudaStream_t st);
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st);
 int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
                         const void *colors, const void *alphas, void *payload, cudaStream_t st);

@@ -71,17 +71,30 @@ __device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dm
 }
 
 // Common prologue: this view's entry count, key shape, and whether `pass` runs.
+// Packed mode (tile + depth + value bits fit 64): pass 0 folds each entry into
+// one u64 `tile << (dbits+vbits) | (depth - dmin) << vbits | value`, so later
+// passes move 8 bytes per entry instead of a 12-byte key/value pair.
 struct PassCtx {
     int64_t e, ntiles;
     unsigned dmin;
-    int dbits, passes;
+    int dbits, passes, vbits;
+    bool packed;
 };
 
-__device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int pass, PassCtx &c) {
+__device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int vbits, int pass,
+                                         PassCtx &c) {
     if (!entries_valid(b.out[v].counters, b.ws[v].entry_capacity, c.e)) return false;
     view_key_shape(b.ws[v].internal, tbits, c.dmin, c.dbits, c.passes);
     c.ntiles = ceil_div(c.e, kSortTile);
+    c.vbits = vbits;
+    c.packed = tbits + c.dbits + vbits <= 64;
     return pass < c.passes;
+}
+
+__device__ __forceinline__ unsigned long long pack_entry(unsigned long long key, unsigned val,
+                                                         const PassCtx &c) {
+    return ((key >> 32) << (c.dbits + c.vbits)) |
+           ((unsigned long long)((unsigned)key - c.dmin) << c.vbits) | (unsigned long long)val;
 }
 
 __device__ __forceinline__ int pass_src(int pass) { return pass & 1; }
@@ -93,14 +106,16 @@ constexpr int kProbe = 4;   // look-back predecessors read per round trip
 // Each warp counts into its own shared histogram with plain shared atomics.
 constexpr int kHistWarps = 4;   // warp histograms per CTA (warps 2w, 2w+1 share one)
 __global__ void __launch_bounds__(kBlock)
-k_sort_hist(const __grid_constant__ Batch b, int tbits) {
+k_sort_hist(const __grid_constant__ Batch b, int tbits, int vbits) {
     __shared__ unsigned h[kHistWarps][4][kBins];   // up to 4 passes counted in smem
     const int v = blockIdx.y;
     PassCtx c;
-    const bool run = pass_ctx(b, v, tbits, 0, c);
+    const bool run = pass_ctx(b, v, tbits, vbits, 0, c);
     const Workspace &ws = b.ws[v];
-    if (blockIdx.x == 0 && threadIdx.x == 0 && c.e <= ws.entry_capacity)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && c.e <= ws.entry_capacity) {
         ws.internal[kSortPasses] = run ? c.passes : 0;
+        ws.internal[kValsBuffer] = (run && !c.packed) ? (c.passes & 1) : 0;
+    }
     if (!run) return;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
@@ -185,7 +200,7 @@ constexpr int kOsWarps = kSortThreads / 32;
 // thread then owns two digits for the prefix over warps, the status publish
 // and the look-back.
 __global__ void __launch_bounds__(kSortThreads, 4)
-k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
+k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass) {
     __shared__ unsigned s_goff[kBins];
     __shared__ unsigned short s_wh[kOsWarps][kBins];
     __shared__ unsigned s_base[kBins];
@@ -193,9 +208,10 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
     __shared__ long long s_tile;
     const int v = blockIdx.y;
     PassCtx c;
-    if (!pass_ctx(b, v, tbits, pass, c)) return;
+    if (!pass_ctx(b, v, tbits, vbits, pass, c)) return;
     const Workspace &ws = b.ws[v];
     const int src = pass_src(pass);
+    const bool need_vals = !c.packed || pass == 0;   // packed passes >= 1 move items only
     const unsigned long long *__restrict__ kin = ws.keys[src];
     const unsigned *__restrict__ vin = ws.vals[src];
     unsigned long long *__restrict__ kout = ws.keys[src ^ 1];
@@ -240,12 +256,18 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
             const int64_t idx = base + k * 32 + lane;
             const bool valid = idx < c.e;
             key[k] = valid ? kin[idx] : ~0ull;
-            val[k] = valid ? vin[idx] : 0u;
+            val[k] = (valid && need_vals) ? vin[idx] : 0u;
+        }
+        if (c.packed && pass == 0) {
+#pragma unroll
+            for (int k = 0; k < kSortItems; ++k) key[k] = pack_entry(key[k], val[k], c);
         }
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             const int64_t idx = base + k * 32 + lane;
-            const unsigned d = idx < c.e ? digit_of(key[k], c.dmin, c.dbits, shift) : (unsigned)kBins;
+            const unsigned d = idx >= c.e ? (unsigned)kBins
+                               : c.packed ? (unsigned)(key[k] >> (c.vbits + shift)) & (kBins - 1)
+                                          : digit_of(key[k], c.dmin, c.dbits, shift);
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
@@ -289,7 +311,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
             if (d >= (unsigned)kBins) continue;
             const unsigned pos = s_base[d] + s_wh[warp][d] + (dr[k] & 0xffffu);
             kout[pos] = key[k];
-            vout[pos] = val[k];
+            if (!c.packed) vout[pos] = val[k];
         }
         __syncthreads();
     }
@@ -297,12 +319,13 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int pass) {
 
 // Ascending in-place sort of a run of equal-key values (shell sort: runs are
 // almost always 2-3 long; a degenerate axis-aligned view can make long ones).
-__device__ void sort_run(unsigned *v, int n) {
+template <typename T>
+__device__ void sort_run(T *v, int n) {
     int gap = 1;
     while (gap < n / 3) gap = 3 * gap + 1;
     for (; gap > 0; gap /= 3)
         for (int a = gap; a < n; ++a) {
-            const unsigned x = v[a];
+            const T x = v[a];
             int c = a;
             while (c >= gap && v[c - gap] > x) {
                 v[c] = v[c - gap];
@@ -312,29 +335,38 @@ __device__ void sort_run(unsigned *v, int n) {
         }
 }
 
-// grid y = view: tile_starts from the boundaries of the sorted keys, and the
-// row-order fix-up of equal-key runs.
+// grid y = view: tile_starts from the boundaries of the sorted keys, the
+// row-order fix-up of equal-key runs, and (packed mode) the entry values
+// unpacked into vals[0] for the compositor.
 __global__ void __launch_bounds__(kBlock)
-k_ranges(const __grid_constant__ Batch b) {
+k_ranges(const __grid_constant__ Batch b, int tbits, int vbits) {
     const int v = blockIdx.y;
     const Workspace &ws = b.ws[v];
     const ViewOut &out = b.out[v];
     const int64_t n_tiles = (int64_t)b.vp[v].tiles_x * b.vp[v].tiles_y;
-    int64_t e;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
     int64_t *starts = ws.tile_starts;
     int64_t *starts2 = out.tile_starts;
-    if (!entries_valid(out.counters, ws.entry_capacity, e)) {   // overflow: empty runs everywhere
-        for (int64_t t = gtid; t <= n_tiles; t += gsz) {
-            starts[t] = 0;
-            if (starts2) starts2[t] = 0;
+    PassCtx c;
+    if (!pass_ctx(b, v, tbits, vbits, 0, c)) {
+        if (!entries_valid(out.counters, ws.entry_capacity, c.e)) {   // overflow: empty runs
+            for (int64_t t = gtid; t <= n_tiles; t += gsz) {
+                starts[t] = 0;
+                if (starts2) starts2[t] = 0;
+            }
+            return;
         }
-        return;
+        c.passes = 0;   // nothing to sort (no entries): the raw buffers are the result
+        c.packed = false;
     }
-    const int fb = sorted_buffer(ws.internal);
-    const unsigned long long *keys = ws.keys[fb];
-    unsigned *vals = ws.vals[fb];
+    const int64_t e = c.e;
+    const bool packed = c.packed;
+    const int kshift = packed ? c.vbits : 0;             // item >> kshift = sort key
+    const int tshift = packed ? c.dbits + c.vbits : 32;  // item >> tshift = tile
+    const unsigned long long vmask = packed ? (1ull << c.vbits) - 1ull : 0ull;
+    unsigned long long *keys = ws.keys[c.passes & 1];
+    unsigned *vals = ws.vals[packed ? 0 : (c.passes & 1)];
     int32_t *entry_out = out.entry_splat;
     constexpr int kR = 4;   // consecutive entries per thread per step (loads in flight)
     for (int64_t i0 = gtid * kR; i0 <= e; i0 += gsz * kR) {
@@ -349,22 +381,31 @@ k_ranges(const __grid_constant__ Batch b) {
             const int64_t i = i0 - 1 + q;
             if (i > e) break;
             const unsigned long long ki = k[q], kp = k[q - 1];
-            const int64_t ti = i < e ? (int64_t)(ki >> 32) : n_tiles;
-            const int64_t tp = i > 0 ? (int64_t)(kp >> 32) : -1;
+            const int64_t ti = i < e ? (int64_t)(ki >> tshift) : n_tiles;
+            const int64_t tp = i > 0 ? (int64_t)(kp >> tshift) : -1;
             for (int64_t t = tp + 1; t <= ti; ++t) {
                 starts[t] = i;
                 if (starts2) starts2[t] = i;
             }
-            if (i >= e || (i > 0 && kp == ki)) continue;   // runs are handled by their first entry
+            if (i >= e || (i > 0 && (kp >> kshift) == (ki >> kshift))) continue;   // run interior
             // Equal keys (same tile, same f32 depth) must end in row order, the
             // reference's stable tie rule: the chain-free projection emits CTA
             // blocks in completion order, so sort each such run by value.
             int64_t j = i + 1;
-            if (k[q + 1] == ki)
-                while (j < e && keys[j] == ki) ++j;
-            if (j - i > 1) sort_run(vals + i, (int)(j - i));
-            if (entry_out)
-                for (int64_t m = i; m < j; ++m) entry_out[m] = (int32_t)vals[m];
+            if ((k[q + 1] >> kshift) == (ki >> kshift))
+                while (j < e && (keys[j] >> kshift) == (ki >> kshift)) ++j;
+            if (packed) {
+                if (j - i > 1) sort_run(keys + i, (int)(j - i));   // value bits are the low bits
+                for (int64_t m = i; m < j; ++m) {
+                    const unsigned val = (unsigned)((m == i && j - i == 1 ? ki : keys[m]) & vmask);
+                    vals[m] = val;
+                    if (entry_out) entry_out[m] = (int32_t)val;
+                }
+            } else {
+                if (j - i > 1) sort_run(vals + i, (int)(j - i));
+                if (entry_out)
+                    for (int64_t m = i; m < j; ++m) entry_out[m] = (int32_t)vals[m];
+            }
         }
     }
 }
@@ -380,32 +421,40 @@ static int num_sms() {
     return cached;
 }
 
-int launch_sort(const Batch &b, cudaStream_t st) {
+static int value_bits(int64_t max_val) {
+    int vb = 1;
+    while (vb < 31 && (1ll << vb) <= max_val) ++vb;
+    return vb;
+}
+
+int launch_sort(const Batch &b, int64_t max_val, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
     const int64_t n_tiles = (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y;
     const int tbits = tile_bits(n_tiles);
+    const int vbits = value_bits(max_val);
     const int max_passes = sort_passes((int)n_tiles);
     const int sms = num_sms();
     const int64_t tiles_cap = b.ws[0].sort_tiles_cap;
     const unsigned hx = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(b.ws[0].entry_capacity, kBlock), std::max(sms * 4 / b.nviews, 1)));
-    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, tbits);
+    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, tbits, vbits);
     trace_mark("sort_hist", st);
     const unsigned ox = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(tiles_cap, std::max<int64_t>(sms * 4 / b.nviews, 1)));
     for (int p = 0; p < max_passes; ++p) {
-        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, tbits, p);
+        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, tbits, vbits, p);
         trace_mark("onesweep", st);
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
-int launch_ranges(const Batch &b, cudaStream_t st) {
+int launch_ranges(const Batch &b, int64_t max_val, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
     const int64_t cap = b.ws[0].entry_capacity;
+    const int64_t n_tiles = (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y;
     const unsigned gx = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(cap + 1, kBlock), std::max(num_sms() * 4 / b.nviews, 1)));
-    k_ranges<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b);
+    k_ranges<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b, tile_bits(n_tiles), value_bits(max_val));
     trace_mark("ranges", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
