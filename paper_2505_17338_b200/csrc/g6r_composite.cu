@@ -469,7 +469,7 @@ int launch_pack_payload(int64_t m, int precision, const void *means2d, const voi
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
-constexpr int kCompositeSub = 2;   // CTAs per 16x16 tile (f32 path)
+constexpr int kCompositeSub = 2;   // CTAs per 16x16 tile
 
 int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
@@ -488,7 +488,8 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     }
     if (vp.precision) {
         if (vp.tile_size == 16)
-            k_composite<double, 256><<<grid, 256, 0, st>>>(b, srt);
+            k_composite<double, 256 / kCompositeSub, kCompositeSub>
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
         else
             k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
