@@ -476,6 +476,13 @@ class DeviceTrainer:
 
     def step(self, view_index: int) -> dict:
         """One iteration on view ``view_index``; returns lr, l1, ssim_loss, total."""
+        row = self.gradients(view_index)
+        self._adam()
+        return row
+
+    def gradients(self, view_index: int) -> dict:
+        """Forward, loss and backward on one view: fills ``self.grads`` (device)
+        and returns the loss row; no parameter update."""
         cam, target = self.views[view_index]
         w, h = int(cam.width), int(cam.height)
         prep = self._prepare()
@@ -500,8 +507,11 @@ class DeviceTrainer:
             self.cap, _ptr(p["mu_p"]), _ptr(p["mu_d"]), _ptr(p["cov_raw"]), _ptr(p["sh"]),
             ctypes.cast(self.ss, ctypes.c_void_p), self.directional_scale, self.w_mode,
             _ptr(gimg), *[_ptr(g[k]) for k in PARAM_GROUPS], _ptr(self.counters), stream))
-        self._adam()
         return {"lr": lr_now, "l1": l1, "ssim_loss": ssim_loss, "total": total}
+
+    def apply_gradients(self):
+        """Adam on ``self.grads`` (skipped when any is non-finite)."""
+        self._adam()
 
     def _adam(self):
         self.flag.zero_()
@@ -567,3 +577,67 @@ def finetune(scene, views, iters: int = 300, loss_cfg: LossConfig = None,
     if checkpoint_path is not None:
         save_checkpoint(out, tr.optimizer_state(), checkpoint_path)
     return out, history
+
+
+# ---------------------------------------------------------------------------
+# Data-parallel fine-tuning (SURVEY.md 8e "Fine-tune (next)")
+# ---------------------------------------------------------------------------
+
+def dp_view_schedule(seed: int, n_views: int, iters: int, world: int) -> np.ndarray:
+    """(iters, world) view indices: iteration t's draws for ranks 0..world-1,
+    from one ``default_rng(seed)`` stream (world = 1 reproduces ``finetune``)."""
+    rng = np.random.default_rng(seed)
+    return np.array([[int(rng.integers(n_views)) for _ in range(world)] for _ in range(iters)],
+                    dtype=np.int64).reshape(iters, world)
+
+
+def allreduce_mean(tensors, group=None):
+    """Average same-dtype tensors across ranks with ONE collective: flatten into
+    a bucket, all-reduce (sum), scale by 1/world, scatter back in place."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    flat = torch.cat([t.reshape(-1) for t in tensors])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    flat.mul_(1.0 / world)
+    k = 0
+    for t in tensors:
+        n = t.numel()
+        t.copy_(flat[k:k + n].view_as(t))
+        k += n
+
+
+def finetune_data_parallel(scene, views, iters: int = 300, loss_cfg: LossConfig = None,
+                           config: RenderConfig = None, seed: int = 0, base_lr: float = 1e-3,
+                           lr_scale: dict = None, group=None):
+    """Data-parallel fine-tuning, one process per GPU (torch.distributed, NCCL
+    over NVLink on B200 nodes): every iteration each rank renders and
+    backpropagates its own view (``dp_view_schedule``), the 40-parameter
+    gradients are averaged with one bucketed all-reduce, and every rank applies
+    the identical Adam step, so parameters stay bit-identical across ranks.
+    With one rank this is ``finetune`` exactly.  Returns ``(scene, history)``
+    on every rank; history losses are averaged over ranks."""
+    import torch
+    import torch.distributed as dist
+    if len(views) == 0:
+        raise InvalidParameterError("finetune needs at least one view")
+    if iters < 0:
+        raise InvalidParameterError(f"iters must be non-negative, got {iters}")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    tr = DeviceTrainer(scene, views, loss_cfg, config, total_steps=max(iters, 1),
+                       base_lr=base_lr, lr_scale=lr_scale)
+    sched = dp_view_schedule(seed, len(views), iters, world)
+    history = []
+    for it in range(iters):
+        row = tr.gradients(int(sched[it, rank]))
+        if world > 1:
+            allreduce_mean([tr.grads[k][:tr.n] for k in PARAM_GROUPS], group)
+            losses = torch.tensor([row["l1"], row["ssim_loss"], row["total"]], dtype=torch.float64,
+                                  device=tr.dev)
+            dist.all_reduce(losses, group=group)
+            l1, ssim_loss, total = (losses / world).tolist()
+            row = {"lr": row["lr"], "l1": l1, "ssim_loss": ssim_loss, "total": total}
+        tr.apply_gradients()
+        history.append({"iteration": it, **row})
+    return tr.result_scene(), history

@@ -52,3 +52,37 @@ def test_broadcast_and_shard_world2(tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert (tmp_path / f"rank{r}").read_text() == "ok"
+
+
+def _dp_worker(rank, world, port, result_dir):
+    """Data-parallel fine-tune host logic: the view schedule is identical on
+    every rank and the bucketed gradient all-reduce averages in place."""
+    from paper_2505_17338_b200 import diffrender as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sched = torch.from_numpy(D.dp_view_schedule(7, 9, 12, world))
+        gathered = [torch.zeros_like(sched) for _ in range(world)]
+        dist.all_gather(gathered, sched)
+        ok = all(torch.equal(g, gathered[0]) for g in gathered)
+        # world-1 column 0 reproduces finetune's single-rank draws
+        rng = np.random.default_rng(7)
+        ok = ok and [int(rng.integers(9)) for _ in range(12)] == D.dp_view_schedule(7, 9, 12, 1)[:, 0].tolist()
+        grads = [torch.full((5, 3), float(rank + 1), dtype=torch.float64),
+                 torch.arange(4, dtype=torch.float64) * (rank + 1)]
+        D.allreduce_mean(grads)
+        mean = sum(r + 1 for r in range(world)) / world
+        ok = ok and torch.equal(grads[0], torch.full((5, 3), mean, dtype=torch.float64))
+        ok = ok and torch.allclose(grads[1], torch.arange(4, dtype=torch.float64) * mean)
+        with open(os.path.join(result_dir, f"dp{rank}"), "w") as fh:
+            fh.write("ok" if ok else "bad")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_data_parallel_finetune_host_logic_world2(tmp_path):
+    world = 2
+    mp.spawn(_dp_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert (tmp_path / f"dp{r}").read_text() == "ok"

@@ -170,3 +170,24 @@ def test_device_ingest_rejects_bad_labels(tmp_path):
     path.write_bytes(bytes(blob))
     with pytest.raises(Exception):
         sceneio.load_scene_device(path)
+
+
+def test_data_parallel_finetune_single_rank_equals_finetune():
+    """One NCCL rank: the data-parallel loop is the reference loop exactly."""
+    import socket
+    import torch.distributed as dist
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        name, fixture, views, iters, seed, kw = FINETUNE_CASES[0]
+        scene, pairs = _finetune_inputs(fixture, views)
+        a, ha = D.finetune(scene, pairs, iters=5, seed=seed)
+        b, hb = D.finetune_data_parallel(scene, pairs, iters=5, seed=seed)
+        assert ha == hb
+        for k in D.PARAM_GROUPS:
+            np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
+    finally:
+        dist.destroy_process_group()
