@@ -110,6 +110,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             double c[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) c[k] = 0.0;
+            bool contrib = false;
             if (active && e < lo + last) {
                 const BwdSplat s = s_sp[j];
                 const double dx = fx - s.mx, dy = fy - s.my;
@@ -137,8 +138,13 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                         sg = sg + s.g * w;
                         sb = sb + s.b * w;
                         sa = sa + w;
+                        contrib = true;
                     }
                 }
+            }
+            if (!__any_sync(0xffffffffu, contrib)) {   // an exact zero row: skip the reduction
+                if (lane == 0) s_hit[warp][j] = 0;
+                continue;
             }
 #pragma unroll
             for (int k = 0; k < 9; ++k) {

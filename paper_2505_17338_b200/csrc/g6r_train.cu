@@ -118,8 +118,10 @@ __global__ void k_sum_partials(const double *__restrict__ part, int n, double *_
 
 // per-window gradients of SsimParts.backward (_ssim.py:86-98) for constant
 // per-window upstream gradients g_lcs, g_cs
-__global__ void k_ssim_bwd_maps(const double *__restrict__ maps, int64_t n, double g_lcs, double g_cs,
-                                double *__restrict__ gm) {
+__global__ void k_ssim_bwd_maps(const double *__restrict__ maps, int64_t n, const double *g_scale,
+                                int last, double *__restrict__ gm) {
+    // per-window upstream gradient of this scale, computed on the device
+    const double g_lcs = last ? *g_scale : 0.0, g_cs = last ? 0.0 : *g_scale;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double ux = maps[i], uy = maps[n + i], b1 = maps[2 * n + i], b2 = maps[3 * n + i];
         const double l = maps[4 * n + i], cs = maps[5 * n + i];
@@ -252,15 +254,58 @@ static LossLayout loss_layout(int h, int w, int scales) {
 
 size_t loss_workspace_bytes(int h, int w) { return loss_layout(h, w, 5).total; }
 
-// sum of a*b (or a) over n doubles, deterministic; result read back to host
-static double dsum(const double *a, const double *b, int64_t n, double *part, double *scal,
-                   cudaStream_t st) {
+// sum of a*b (or a) over n doubles into *out (device), deterministic
+static void dsum(const double *a, const double *b, int64_t n, double *part, double *out,
+                 cudaStream_t st) {
     k_partials<<<kRedBlocks, 256, 0, st>>>(a, b, n, part);
-    k_sum_partials<<<1, 32, 0, st>>>(part, kRedBlocks, scal);
-    double out = 0.0;
-    cudaMemcpyAsync(&out, scal, sizeof(double), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    return out;
+    k_sum_partials<<<1, 32, 0, st>>>(part, kRedBlocks, out);
+}
+
+// Scalar slots of the loss workspace (device doubles).
+constexpr int kSlotL1 = 0, kSlotParts = 1;   // l1 sum; total, l1, ssim_loss
+constexpr int kSlotChan = 8, kChanStride = 16;   // per channel: sums[5], value, g[5]
+
+struct ScaleWeights {
+    double w[5], count[5];
+};
+
+// MS-SSIM value and per-scale window gradients of one channel (_ssim.py:163-198):
+// terms = means (clamped at 0 for the multi-scale product), value = prod(terms^w),
+// g[j] = value * w_j / terms_j / count_j (0 where the reference skips the scale).
+__global__ void k_msssim_scalars(double *chan, int ns, ScaleWeights sw) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double terms[5];
+    for (int j = 0; j < ns; ++j) terms[j] = chan[j] / sw.count[j];
+    double *g = chan + 6;
+    if (ns == 1) {
+        chan[5] = terms[0];
+        g[0] = 1.0 / sw.count[0];
+        return;
+    }
+    double value = 1.0;
+    for (int j = 0; j < ns; ++j) {
+        terms[j] = terms[j] > 0.0 ? terms[j] : 0.0;
+        value *= pow(terms[j], sw.w[j]);
+    }
+    chan[5] = value;
+    for (int j = 0; j < ns; ++j)
+        g[j] = (value > 0.0 && terms[j] > 0.0) ? value * sw.w[j] / terms[j] / sw.count[j] : 0.0;
+}
+
+__global__ void k_loss_parts(double *scal, int use_ssim, double lambda_l1, double lambda_ssim,
+                             double n_l1) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double l1 = scal[kSlotL1] / n_l1;
+    double ssim_value = 0.0;
+    if (use_ssim) {
+        double total = 0.0;
+        for (int c = 0; c < 3; ++c) total += scal[kSlotChan + c * kChanStride + 5];
+        ssim_value = total / 3.0;
+    }
+    const double ssim_loss = use_ssim ? 1.0 - ssim_value : 0.0;
+    scal[kSlotParts] = lambda_l1 * l1 + lambda_ssim * ssim_loss;
+    scal[kSlotParts + 1] = l1;
+    scal[kSlotParts + 2] = ssim_loss;
 }
 
 int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
@@ -284,33 +329,33 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
     // L1 (diffrender.py:126-129)
     double *absd = reinterpret_cast<double *>(base + L.absd);
     k_l1<<<grid_for(hw * 3), 256, 0, st>>>(pred, tgt, tc, hw, lambda_l1 / (double)(hw * 3), grad, absd);
-    const double l1 = dsum(absd, nullptr, hw * 3, part, scal, st) / (double)(hw * 3);
-    double ssim_value = 0.0;
+    dsum(absd, nullptr, hw * 3, part, scal + kSlotL1, st);
     if (lambda_ssim > 0.0) {
         // effective_scales (_ssim.py:116-120)
         const int ns = std::min(h, w) < (1 << (scales - 1)) * kWin ? 1 : scales;
-        std::vector<double> wts(ns);
+        ScaleWeights sw{};
         double wsum = 0.0;
         for (int j = 0; j < ns; ++j) wsum += weights_in[j];
-        for (int j = 0; j < ns; ++j) wts[j] = weights_in[j] / wsum;
-        double total = 0.0;
+        for (int j = 0; j < ns; ++j) sw.w[j] = weights_in[j] / wsum;
+        int hs[5], wsz[5];
+        hs[0] = h;
+        wsz[0] = w;
+        for (int j = 1; j < ns; ++j) {
+            hs[j] = hs[j - 1] / 2;
+            wsz[j] = wsz[j - 1] / 2;
+        }
+        for (int j = 0; j < ns; ++j)
+            sw.count[j] = (double)((int64_t)(hs[j] - kWin + 1) * (wsz[j] - kWin + 1));
         for (int c = 0; c < 3; ++c) {
-            int hs[5], wsz[5];
+            double *chan = scal + kSlotChan + c * kChanStride;
             double *xs[5], *ys[5], *mp[5];
-            hs[0] = h;
-            wsz[0] = w;
             for (int j = 0; j < ns; ++j) {
                 xs[j] = reinterpret_cast<double *>(base + L.x[j]);
                 ys[j] = reinterpret_cast<double *>(base + L.y[j]);
                 mp[j] = reinterpret_cast<double *>(base + L.maps[j]);
-                if (j > 0) {
-                    hs[j] = hs[j - 1] / 2;
-                    wsz[j] = wsz[j - 1] / 2;
-                }
             }
             k_extract<<<grid_for(hw), 256, 0, st>>>(pred, 4, c, hw, xs[0]);
             k_extract<<<grid_for(hw), 256, 0, st>>>(tgt, tc, c, hw, ys[0]);
-            double terms[5], counts[5];
             for (int j = 0; j < ns; ++j) {
                 const int hj = hs[j], wj = wsz[j];
                 const int64_t hwj = (int64_t)hj * wj;
@@ -322,23 +367,14 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
                 k_corr1d<<<grid_for(5 * (int64_t)hv * wj), 256, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0);
                 k_corr1d<<<grid_for(5 * nv), 256, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0);
                 k_ssim_maps<<<grid_for(nv), 256, 0, st>>>(stats, nv, mp[j]);
-                const bool last = j == ns - 1;
-                const double s = last ? dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, part, scal, st)
-                                      : dsum(mp[j] + 5 * nv, nullptr, nv, part, scal, st);
-                terms[j] = s / (double)nv;
-                counts[j] = (double)nv;
+                if (j == ns - 1) dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, part, chan + j, st);
+                else dsum(mp[j] + 5 * nv, nullptr, nv, part, chan + j, st);
                 if (j + 1 < ns) {
                     k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(xs[j], hj, wj, xs[j + 1]);
                     k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(ys[j], hj, wj, ys[j + 1]);
                 }
             }
-            double value;
-            if (ns == 1) {
-                value = terms[0];
-            } else {
-                value = 1.0;
-                for (int j = 0; j < ns; ++j) value *= std::pow(std::max(terms[j], 0.0), wts[j]);
-            }
+            k_msssim_scalars<<<1, 32, 0, st>>>(chan, ns, sw);
             // backward from the coarsest scale (_ssim.py:175-198)
             double *g = reinterpret_cast<double *>(base + L.g);
             double *g2 = g + hw;
@@ -352,37 +388,21 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
                     k_pool2_adjoint<<<grid_for(hwj), 256, 0, st>>>(g, hj, wj, g2);
                     std::swap(g, g2);
                 }
-                double g_lcs = 0.0, g_cs = 0.0;
-                bool go = false;
-                if (ns == 1) {
-                    g_lcs = 1.0 / counts[0];
-                    go = true;
-                } else if (value > 0.0 && terms[j] > 0.0) {
-                    const double per = value * wts[j] / terms[j] / counts[j];
-                    if (j == ns - 1) g_lcs = per;
-                    else g_cs = per;
-                    go = true;
-                }
-                if (go) {
-                    double *gm = reinterpret_cast<double *>(base + L.gm);
-                    double *tmp = reinterpret_cast<double *>(base + L.tmp);
-                    double *adj = reinterpret_cast<double *>(base + L.adj);
-                    k_ssim_bwd_maps<<<grid_for(nv), 256, 0, st>>>(mp[j], nv, g_lcs, g_cs, gm);
-                    k_corr1d<<<grid_for(3 * (int64_t)hj * wv), 256, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
-                    k_corr1d<<<grid_for(3 * hwj), 256, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
-                    k_ssim_bwd_combine<<<grid_for(hwj), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g);
-                }
+                double *gm = reinterpret_cast<double *>(base + L.gm);
+                double *tmp = reinterpret_cast<double *>(base + L.tmp);
+                double *adj = reinterpret_cast<double *>(base + L.adj);
+                k_ssim_bwd_maps<<<grid_for(nv), 256, 0, st>>>(mp[j], nv, chan + 6 + j, j == ns - 1, gm);
+                k_corr1d<<<grid_for(3 * (int64_t)hj * wv), 256, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
+                k_corr1d<<<grid_for(3 * hwj), 256, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
+                k_ssim_bwd_combine<<<grid_for(hwj), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g);
             }
             // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
             k_axpy_channel<<<grid_for(hw), 256, 0, st>>>(g, hw, c, -lambda_ssim / 3.0, grad);
-            total += value;
         }
-        ssim_value = total / 3.0;
     }
-    const double ssim_loss = lambda_ssim > 0.0 ? 1.0 - ssim_value : 0.0;
-    parts[0] = lambda_l1 * l1 + lambda_ssim * ssim_loss;
-    parts[1] = l1;
-    parts[2] = ssim_loss;
+    k_loss_parts<<<1, 32, 0, st>>>(scal, lambda_ssim > 0.0, lambda_l1, lambda_ssim, (double)(hw * 3));
+    cudaMemcpyAsync(parts, scal + kSlotParts, 3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);   // the one read-back of the call
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
