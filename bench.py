@@ -372,13 +372,16 @@ def run_b200(args):
             "overflowed_views": overflow,
             "prep_ms": prep_ms, "broadcast_ms": bcast_ms,
             "view_algorithmic_gbs": view_bytes * views_per_s / world / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_composite<float>",
+            "roofline": {"bound": "hbm", "kernel": "k_composite<float,128,2>",
                          "achieved": comp_gbs, "peak": peak, "unit": "GB/s",
                          "frac": comp_gbs / peak, "traffic": traffic,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": comp_bytes,
                          "note": "compositor is issue-bound (FP32+FP64 per pixel x entry); "
-                                 "bytes = 40 E + 16 HW per view (SURVEY 8d)"},
+                                 "bytes = 40 E + 16 HW per view (SURVEY 8d); launch duration "
+                                 "from CUDA events around each batch's compositor launch in a "
+                                 "second, single-stream pass over the same views (the timed pass "
+                                 "overlaps batches on two streams)"},
             "e2e": {"value": world * V / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 136, "d2h_bytes_per_step": H * W * 16 + 128,
                     "api": "paper_2505_17338_b200.raster.render_batch (numpy images out, "
