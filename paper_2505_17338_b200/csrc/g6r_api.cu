@@ -42,7 +42,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_counts, total;
+        sort_counts, rect, chunk_hist, tile_total, total;
     int64_t sort_tiles_cap;
 };
 
@@ -62,17 +62,25 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + (tiles + 1) * sizeof(int64_t));
     L.payload = o;
     o = align_up(o + (size_t)n * (precision ? sizeof(PayloadF64) : sizeof(PayloadF32)));
+    // the sort buffers hold either the E tile entries or the n splat keys
+    const int64_t items = std::max<int64_t>(cap, n);
     L.keys0 = o;
-    o = align_up(o + (size_t)cap * 8);
+    o = align_up(o + (size_t)items * 8);
     L.keys1 = o;
-    o = align_up(o + (size_t)cap * 8);
+    o = align_up(o + (size_t)items * 8);
     L.vals0 = o;
     o = align_up(o + (size_t)cap * 4);
     L.vals1 = o;
     o = align_up(o + (size_t)cap * 4);
-    L.sort_tiles_cap = ceil_div(cap > 0 ? cap : 1, kSortTile);
+    L.sort_tiles_cap = ceil_div(items > 0 ? items : 1, kSortTile);
     L.sort_counts = o;
     o = align_up(o + (size_t)kMaxPasses * L.sort_tiles_cap * kBins * sizeof(unsigned));
+    L.rect = o;
+    o = align_up(o + (size_t)n * sizeof(uint2));
+    L.chunk_hist = o;
+    o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, kChunkSplats) * tiles * sizeof(unsigned));
+    L.tile_total = o;
+    o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -90,6 +98,9 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.vals[0] = reinterpret_cast<unsigned *>(b + L.vals0);
     w.vals[1] = reinterpret_cast<unsigned *>(b + L.vals1);
     w.sort_counts = reinterpret_cast<unsigned *>(b + L.sort_counts);
+    w.rect = reinterpret_cast<uint2 *>(b + L.rect);
+    w.chunk_hist = reinterpret_cast<unsigned *>(b + L.chunk_hist);
+    w.tile_total = reinterpret_cast<unsigned *>(b + L.tile_total);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;
     return w;
@@ -238,15 +249,20 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     }
     if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     prof_mark(prof, 0, st);
-    if (launch_project(*scene, mask, b, nviews == 1 ? splats : nullptr, true, st))
-        return cuda_check("project");
+    const g6r_splat_out *so = nviews == 1 ? splats : nullptr;
+    const bool splat_sort = !projection_ordered(b, so, true) && splat_sort_applies(b);
+    if (launch_project(*scene, mask, b, so, true, st)) return cuda_check("project");
     prof_mark(prof, 1, st);
-    // (Sorting the batch in L2-sized sub-batches was measured slower: the extra
-    //  launches cost more than the HBM traffic they save.)
-    if (launch_sort(b, scene->n, st)) return cuda_check("sort");
-    prof_mark(prof, 2, st);
-    if (launch_ranges(b, scene->n, st)) return cuda_check("ranges");
-    prof_mark(prof, 3, st);
+    if (splat_sort) {   // depth sort of the splats + order-preserving tile expansion
+        if (launch_splat_sort(b, scene->n, st)) return cuda_check("sort");
+        prof_mark(prof, 2, st);
+        prof_mark(prof, 3, st);
+    } else {            // tile entries: radix sort of (tile, depth) keys, then ranges
+        if (launch_sort(b, scene->n, st)) return cuda_check("sort");
+        prof_mark(prof, 2, st);
+        if (launch_ranges(b, scene->n, st)) return cuda_check("ranges");
+        prof_mark(prof, 3, st);
+    }
     if (launch_composite(b, true, st)) return cuda_check("composite");
     prof_mark(prof, 4, st);
     if (prof && prof->used < prof->max_batches) {

@@ -27,9 +27,19 @@ struct Workspace {
     unsigned *sort_counts;          // kMaxPasses x tiles_cap x kBins per-tile digit counts
     int64_t *tile_starts;           // T+1 (internal copy)
     int4 *splat_rect;               // optional (backward): per splat (entry offset, x0, y0, wx)
+    uint2 *rect;                    // splat-sort path: per scene row (x0 | y0 << 16, wx | hy << 16)
+    unsigned *chunk_hist;           // splat-sort path: per chunk of sorted splats, T tile counts
+    unsigned *tile_total;           // splat-sort path: T entry counts
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
 };
+
+// Splat-level sort (g6r_tiles.cu): the hot-path projection writes one depth key
+// and one tile rect per scene row; the rows are radix-sorted by depth and then
+// expanded into tile runs by an order-preserving partition in chunks of
+// kChunkSplats sorted splats.
+constexpr int kChunkSplats = 2048;
+constexpr int kMaxSplatSortTiles = 4096;   // larger tile grids use the entry sort
 
 struct ViewParams {
     double pos[3];
@@ -85,6 +95,14 @@ int launch_duplicate(int64_t m, const double *means2d, const int32_t *radii, con
 int launch_sort(const Batch &b, int64_t max_val, cudaStream_t st);
 // per-tile ranges into ws.tile_starts (+ optional copies of starts / entry_splat)
 int launch_ranges(const Batch &b, int64_t max_val, cudaStream_t st);
+// Which projection/sort a render uses: ordered (compacted SplatBatch outputs,
+// entry sort) when splat outputs or per-splat rects are requested; otherwise
+// the splat-level sort when the tile grid fits kMaxSplatSortTiles.
+bool projection_ordered(const Batch &b, const g6r_splat_out *splats, bool write_entries);
+bool splat_sort_applies(const Batch &b);
+// splat-level sort + tile partition (hot path); n = scene rows
+int launch_splat_sort(const Batch &b, int64_t n, cudaStream_t st);
+int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st);
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st);
 int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
                         const void *colors, const void *alphas, void *payload, cudaStream_t st);

@@ -345,7 +345,11 @@ __device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *
 // entry array is then in CTA-completion order, so equal sort keys are put
 // back in row order after the sort (k_ranges), which is the reference's tie
 // rule (rows ascend with the compacted index).
-template <bool kF64, bool kOrdered>
+//
+// kSplatKeys (hot path, unordered): no tile entries at all -- every scene row
+// writes one depth key (f32 depth bits, all-ones for rows not drawn) and its
+// tile rect, for the splat-level sort in g6r_tiles.cu.
+template <bool kF64, bool kOrdered, bool kSplatKeys = false>
 __global__ void __launch_bounds__(kBlock)
 k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_splat_out so,
           int write_entries, double sh_c0, double sh_c1) {
@@ -464,6 +468,20 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
         }
         }
         if (kOrdered && ws.splat_rect) ws.splat_rect[m] = make_int4((int)(e_base + le), x0, y0, wx);
+    }
+    if (kSplatKeys) {
+        if (i < n) {
+            ws.keys[0][i] = kept ? (unsigned long long)db : 0xffffffffull;
+            ws.rect[i] = kept ? make_uint2((unsigned)x0 | ((unsigned)y0 << 16),
+                                           (unsigned)wx | ((unsigned)hy << 16))
+                              : make_uint2(0u, 0u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 6 && s_fate[threadIdx.x])
+            atomicAdd((unsigned long long *)&counters[G6R_CNT_FATE + threadIdx.x],
+                      (unsigned long long)s_fate[threadIdx.x]);
+        if (threadIdx.x == 0 && s_dext[1]) note_depth_extrema(ws.internal, s_dext[0], s_dext[1]);
+        return;
     }
     // Duplication, hybrid: a splat with few tiles writes its own entries (row-
     // major over its rect); larger ones are queued and emitted by the whole CTA.
@@ -608,6 +626,16 @@ __global__ void k_stage2(int64_t n, const double *view, const double *mean_adj, 
 static const double kShC0 = 0.28209479177387814;   // core.py:25
 static const double kShC1 = 0.4886025119029199;    // core.py:26
 
+bool projection_ordered(const Batch &b, const g6r_splat_out *splats, bool write_entries) {
+    if (!write_entries || b.ws[0].splat_rect) return true;
+    return splats && (splats->gids || splats->means2d || splats->conics || splats->colors ||
+                      splats->alphas || splats->depths || splats->radii || splats->stage);
+}
+
+bool splat_sort_applies(const Batch &b) {
+    return (int64_t)b.vp[0].tiles_x * b.vp[0].tiles_y <= kMaxSplatSortTiles;
+}
+
 int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
                    const g6r_splat_out *splats, bool write_entries, cudaStream_t st) {
     g6r_splat_out so{};
@@ -615,15 +643,19 @@ int launch_project(const g6r_scene &scene, uint32_t mask, const Batch &b,
     if (scene.n == 0 || b.nviews == 0) return G6R_OK;
     const dim3 grid((unsigned)b.nviews, (unsigned)ceil_div(scene.n, kBlock));
     // compacted (ordered) only when SplatBatch-shaped outputs or rects are wanted
-    const bool ordered = !write_entries || so.gids || so.means2d || so.conics || so.colors ||
-                         so.alphas || so.depths || so.radii || so.stage || b.ws[0].splat_rect;
+    const bool ordered = projection_ordered(b, splats, write_entries);
+    const bool keys = !ordered && splat_sort_applies(b);
     const bool f64 = b.vp[0].precision != 0;
     if (f64 && ordered)
         k_project<true, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    else if (f64 && keys)
+        k_project<true, false, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else if (f64)
         k_project<true, false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else if (ordered)
         k_project<false, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
+    else if (keys)
+        k_project<false, false, true><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     else
         k_project<false, false><<<grid, kBlock, 0, st>>>(scene, mask, b, so, write_entries, kShC0, kShC1);
     trace_mark("project", st);

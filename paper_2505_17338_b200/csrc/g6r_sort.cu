@@ -53,20 +53,29 @@ __device__ __forceinline__ bool entries_valid(const int64_t *counters, int64_t c
 }
 
 // (dmin, dbits, passes) of a view from the projection's depth-bit extrema.
-__device__ __forceinline__ void view_key_shape(const long long *internal, int tbits, unsigned &dmin,
-                                               int &dbits, int &passes) {
+// With `sentinel` (splat sort) one more code, span + 1, is reserved for rows
+// that were not drawn (key all-ones), so they sort after every drawn splat.
+__device__ __forceinline__ void view_key_shape(const long long *internal, int tbits, bool sentinel,
+                                               unsigned &dmin, unsigned &dtop, int &dbits,
+                                               int &passes) {
     const unsigned lo = ~(unsigned)internal[kDepthMinInv];
     const unsigned hi = (unsigned)internal[kDepthMax];
     const unsigned span = hi >= lo ? hi - lo : 0u;
     dmin = hi >= lo ? lo : 0u;
-    dbits = span ? 32 - __clz(span) : 0;
+    dtop = span + (sentinel ? 1u : 0u);   // largest compressed depth code
+    dbits = dtop ? 32 - __clz(dtop) : 0;
     passes = (tbits + dbits + kRadixBits - 1) / kRadixBits;
 }
 
-__device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dmin, int dbits,
-                                             int shift) {
+__device__ __forceinline__ unsigned depth_code(unsigned long long key, unsigned dmin, unsigned dtop) {
+    const unsigned d = (unsigned)key - dmin;
+    return d < dtop ? d : dtop;   // clamps the not-drawn sentinel (and only it)
+}
+
+__device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dmin, unsigned dtop,
+                                             int dbits, int shift) {
     const unsigned long long k2 =
-        ((key >> 32) << dbits) | (unsigned long long)((unsigned)key - dmin);
+        ((key >> 32) << dbits) | (unsigned long long)depth_code(key, dmin, dtop);
     return (unsigned)(k2 >> shift) & (kBins - 1);
 }
 
@@ -74,17 +83,24 @@ __device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dm
 // Packed mode (tile + depth + value bits fit 64): pass 0 folds each entry into
 // one u64 `tile << (dbits+vbits) | (depth - dmin) << vbits | value`, so later
 // passes move 8 bytes per entry instead of a 12-byte key/value pair.
+// Splat mode (splat_n > 0): the items are the scene's n rows (key = f32 depth
+// bits or the not-drawn sentinel, value = row), sorted by depth alone.
 struct PassCtx {
     int64_t e, ntiles;
-    unsigned dmin;
+    unsigned dmin, dtop;
     int dbits, passes, vbits;
-    bool packed;
+    bool packed, splat;
 };
 
 __device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int vbits, int pass,
-                                         PassCtx &c) {
+                                         PassCtx &c, int64_t splat_n = 0) {
     if (!entries_valid(b.out[v].counters, b.ws[v].entry_capacity, c.e)) return false;
-    view_key_shape(b.ws[v].internal, tbits, c.dmin, c.dbits, c.passes);
+    c.splat = splat_n > 0;
+    if (c.splat) {
+        c.e = splat_n;
+        tbits = 0;
+    }
+    view_key_shape(b.ws[v].internal, tbits, c.splat, c.dmin, c.dtop, c.dbits, c.passes);
     c.ntiles = ceil_div(c.e, kSortTile);
     c.vbits = vbits;
     c.packed = tbits + c.dbits + vbits <= 64;
@@ -94,7 +110,7 @@ __device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int v
 __device__ __forceinline__ unsigned long long pack_entry(unsigned long long key, unsigned val,
                                                          const PassCtx &c) {
     return ((key >> 32) << (c.dbits + c.vbits)) |
-           ((unsigned long long)((unsigned)key - c.dmin) << c.vbits) | (unsigned long long)val;
+           ((unsigned long long)depth_code(key, c.dmin, c.dtop) << c.vbits) | (unsigned long long)val;
 }
 
 __device__ __forceinline__ int pass_src(int pass) { return pass & 1; }
@@ -106,12 +122,15 @@ constexpr int kProbe = 4;   // look-back predecessors read per round trip
 // Each warp counts into its own shared histogram with plain shared atomics.
 constexpr int kHistWarps = 4;   // warp histograms per CTA (warps 2w, 2w+1 share one)
 __global__ void __launch_bounds__(kBlock)
-k_sort_hist(const __grid_constant__ Batch b, int tbits, int vbits) {
+k_sort_hist(const __grid_constant__ Batch b, int tbits, int vbits, int64_t splat_n) {
     __shared__ unsigned h[kHistWarps][4][kBins];   // up to 4 passes counted in smem
     const int v = blockIdx.y;
     PassCtx c;
-    const bool run = pass_ctx(b, v, tbits, vbits, 0, c);
+    const bool run = pass_ctx(b, v, tbits, vbits, 0, c, splat_n);
     const Workspace &ws = b.ws[v];
+    if (splat_n > 0 && blockIdx.x == 0 && threadIdx.x == 0 &&
+        b.out[v].counters[G6R_CNT_ENTRIES] > ws.entry_capacity)
+        b.out[v].counters[G6R_CNT_OVERFLOW] = 1;   // the entries will not fit: skip the view
     if (blockIdx.x == 0 && threadIdx.x == 0 && c.e <= ws.entry_capacity) {
         ws.internal[kSortPasses] = run ? c.passes : 0;
         ws.internal[kValsBuffer] = (run && !c.packed) ? (c.passes & 1) : 0;
@@ -144,7 +163,7 @@ k_sort_hist(const __grid_constant__ Batch b, int tbits, int vbits) {
             for (int q = 0; q < kH; ++q) {
                 if (i0 + (int64_t)q * blockDim.x >= c.e) break;
                 for (int p = 0; p < np; ++p)
-                    atomicAdd(&h[hw][p][digit_of(key[q], c.dmin, c.dbits, kRadixBits * (p0 + p))], 1u);
+                    atomicAdd(&h[hw][p][digit_of(key[q], c.dmin, c.dtop, c.dbits, kRadixBits * (p0 + p))], 1u);
             }
         }
         __syncthreads();
@@ -200,7 +219,7 @@ constexpr int kOsWarps = kSortThreads / 32;
 // thread then owns two digits for the prefix over warps, the status publish
 // and the look-back.
 __global__ void __launch_bounds__(kSortThreads, 4)
-k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass) {
+k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int64_t splat_n) {
     __shared__ unsigned s_goff[kBins];
     __shared__ unsigned short s_wh[kOsWarps][kBins];
     __shared__ unsigned s_base[kBins];
@@ -208,7 +227,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass) {
     __shared__ long long s_tile;
     const int v = blockIdx.y;
     PassCtx c;
-    if (!pass_ctx(b, v, tbits, vbits, pass, c)) return;
+    if (!pass_ctx(b, v, tbits, vbits, pass, c, splat_n)) return;
     const Workspace &ws = b.ws[v];
     const int src = pass_src(pass);
     const bool need_vals = !c.packed || pass == 0;   // packed passes >= 1 move items only
@@ -256,7 +275,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass) {
             const int64_t idx = base + k * 32 + lane;
             const bool valid = idx < c.e;
             key[k] = valid ? kin[idx] : ~0ull;
-            val[k] = (valid && need_vals) ? vin[idx] : 0u;
+            val[k] = (valid && need_vals) ? (c.splat ? (unsigned)idx : vin[idx]) : 0u;
         }
         if (c.packed && pass == 0) {
 #pragma unroll
@@ -267,7 +286,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass) {
             const int64_t idx = base + k * 32 + lane;
             const unsigned d = idx >= c.e ? (unsigned)kBins
                                : c.packed ? (unsigned)(key[k] >> (c.vbits + shift)) & (kBins - 1)
-                                          : digit_of(key[k], c.dmin, c.dbits, shift);
+                                          : digit_of(key[k], c.dmin, c.dtop, c.dbits, shift);
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
@@ -437,15 +456,38 @@ int launch_sort(const Batch &b, int64_t max_val, cudaStream_t st) {
     const int64_t tiles_cap = b.ws[0].sort_tiles_cap;
     const unsigned hx = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(b.ws[0].entry_capacity, kBlock), std::max(sms * 4 / b.nviews, 1)));
-    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, tbits, vbits);
+    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, tbits, vbits, 0);
     trace_mark("sort_hist", st);
     const unsigned ox = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(tiles_cap, std::max<int64_t>(sms * 4 / b.nviews, 1)));
     for (int p = 0; p < max_passes; ++p) {
-        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, tbits, vbits, p);
+        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, tbits, vbits, p, 0);
         trace_mark("onesweep", st);
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+// Splat-level sort: depth radix passes over the n scene rows (the not-drawn
+// rows sort last), then the order-preserving tile partition (g6r_tiles.cu).
+int launch_splat_sort(const Batch &b, int64_t n, cudaStream_t st) {
+    if (b.nviews == 0) return G6R_OK;
+    if (n == 0) return launch_tile_partition(b, n, 1, st);   // empty runs
+    const int vbits = value_bits(n);
+    const int max_passes = (32 + 1 + kRadixBits - 1) / kRadixBits;   // depth bits + sentinel
+    const int sms = num_sms();
+    const unsigned hx = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1), kBlock), std::max(sms * 4 / b.nviews, 1)));
+    k_sort_hist<<<dim3(hx, b.nviews), kBlock, 0, st>>>(b, 0, vbits, std::max<int64_t>(n, 1));
+    trace_mark("sort_hist", st);
+    const unsigned ox = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1), kSortTile),
+                             std::max<int64_t>(sms * 4 / b.nviews, 1)));
+    for (int p = 0; p < max_passes; ++p) {
+        k_onesweep<<<dim3(ox, b.nviews), kSortThreads, 0, st>>>(b, 0, vbits, p, std::max<int64_t>(n, 1));
+        trace_mark("onesweep", st);
+    }
+    if (cudaGetLastError() != cudaSuccess) return G6R_ECUDA;
+    return launch_tile_partition(b, n, vbits, st);
 }
 
 int launch_ranges(const Batch &b, int64_t max_val, cudaStream_t st) {
