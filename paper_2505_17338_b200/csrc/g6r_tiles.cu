@@ -189,6 +189,7 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     unsigned short *s_rank = reinterpret_cast<unsigned short *>(s_rwin + kWindow);   // [kWindow]
     unsigned *s_base = reinterpret_cast<unsigned *>(s_rank + kWindow);         // [T]
     unsigned short *s_cnt = reinterpret_cast<unsigned short *>(s_base + c.tiles);   // [warps][T]
+    unsigned short *s_tot = s_cnt + kScatterWarps * c.tiles;                        // [T]
     const unsigned *chunk_off = ws.chunk_hist + (int64_t)blockIdx.x * c.tiles;
     for (int t = threadIdx.x; t < c.tiles; t += blockDim.x)
         s_base[t] = (unsigned)ws.tile_starts[t] + chunk_off[t];
@@ -237,10 +238,19 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
                 const int cnt = wx * hy;
                 const int k_lo = w0 > off ? w0 - off : 0;
                 const int k_hi = off + cnt < w0 + wn ? cnt : w0 + wn - off;
-                for (int k = k_lo; k < k_hi; ++k) {
-                    const int qy = k / wx;
-                    s_ewin[off + k - w0] = (unsigned)((y0 + qy) * c.tiles_x + x0 + (k - qy * wx));
-                    s_rwin[off + k - w0] = row[q];
+                if (k_lo < k_hi) {   // row-major walk of the rect from entry k_lo
+                    int qy = k_lo / wx, qx = k_lo - qy * wx;
+                    unsigned t = (unsigned)((y0 + qy) * c.tiles_x + x0 + qx);
+                    for (int k = k_lo; k < k_hi; ++k) {
+                        s_ewin[off + k - w0] = t;
+                        s_rwin[off + k - w0] = row[q];
+                        if (++qx == wx) {
+                            qx = 0;
+                            t += (unsigned)(c.tiles_x - wx + 1);
+                        } else {
+                            ++t;
+                        }
+                    }
                 }
                 off += cnt;
             }
@@ -263,31 +273,29 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
                 __syncwarp();
             }
             __syncthreads();
-            // scatter: tile base + earlier warps' counts + rank
-            for (int slot = threadIdx.x; slot < wn; slot += blockDim.x) {
-                const unsigned t = s_ewin[slot];
-                const int w_of = slot / kWinPerWarp;
-                unsigned before = 0;
-                for (int w = 0; w < w_of; ++w) before += s_cnt[w * c.tiles + t];
-                vals[s_base[t] + before + s_rank[slot]] = s_rwin[slot];
-            }
-            __syncthreads();
-            // the window's last entry of each tile advances its base, clears counters
-            for (int slot = threadIdx.x; slot < wn; slot += blockDim.x) {
-                const unsigned t = s_ewin[slot];
-                const int w_of = slot / kWinPerWarp;
-                unsigned sum = 0, after = 0;
+            // per tile: the warp counts become exclusive offsets (warps in order)
+            for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) {
+                unsigned run = 0;
 #pragma unroll
                 for (int w = 0; w < kScatterWarps; ++w) {
                     const unsigned x = s_cnt[w * c.tiles + t];
-                    sum += x;
-                    after += w > w_of ? x : 0u;
+                    s_cnt[w * c.tiles + t] = (unsigned short)run;
+                    run += x;
                 }
-                if (after == 0u && s_rank[slot] + 1u == s_cnt[w_of * c.tiles + t]) {
-                    s_base[t] += sum;
+                s_tot[t] = (unsigned short)run;
+            }
+            __syncthreads();
+            // scatter: tile base + warp offset + rank
+            for (int slot = threadIdx.x; slot < wn; slot += blockDim.x) {
+                const unsigned t = s_ewin[slot];
+                vals[s_base[t] + s_cnt[(slot / kWinPerWarp) * c.tiles + t] + s_rank[slot]] = s_rwin[slot];
+            }
+            __syncthreads();
+            // advance the bases by this window's counts and clear the counters
+            for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) {
+                s_base[t] += s_tot[t];
 #pragma unroll
-                    for (int w = 0; w < kScatterWarps; ++w) s_cnt[w * c.tiles + t] = 0;
-                }
+                for (int w = 0; w < kScatterWarps; ++w) s_cnt[w * c.tiles + t] = 0;
             }
             __syncthreads();
         }
@@ -300,13 +308,14 @@ int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st)
     const int64_t chunks = ceil_div(n > 0 ? n : 1, kChunkSplats);
     const unsigned long long vmask = (1ull << vbits) - 1ull;
     const size_t count_smem = (size_t)tiles * sizeof(unsigned);
-    const size_t scatter_smem = kScatterStatic + (size_t)tiles * (sizeof(unsigned) + kScatterWarps * sizeof(unsigned short));
+    const size_t scatter_smem =
+        kScatterStatic + (size_t)tiles * (sizeof(unsigned) + (kScatterWarps + 1) * sizeof(unsigned short));
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(k_chunk_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kMaxSplatSortTiles * sizeof(unsigned)));
         cudaFuncSetAttribute(k_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kScatterStatic + kMaxSplatSortTiles * (sizeof(unsigned) + kScatterWarps * sizeof(unsigned short))));
+                             (int)(kScatterStatic + kMaxSplatSortTiles * (sizeof(unsigned) + (kScatterWarps + 1) * sizeof(unsigned short))));
         attrs = true;
     }
     const dim3 cgrid((unsigned)chunks, (unsigned)b.nviews);
