@@ -450,3 +450,28 @@ def test_f64_batched_views_match_single_renders():
     imgs, _ = raster.render_views(s, cams, config=cfg)
     for k, cam in enumerate(cams):
         np.testing.assert_array_equal(imgs[k].cpu().numpy(), raster.render(s, cam, config=cfg))
+
+
+def test_splat_sort_windows_and_large_grids_match_entry_sort(oracle):
+    """Hot path (splat-level sort) vs the entry sort (render_with_state) on a
+    scene with a few huge splats -- rounds whose entries span several 4096-entry
+    windows -- at 1024x1024 (4096 tiles, splat sort) and at 1040x1040 (4225
+    tiles, entry sort for both)."""
+    s = scenes.random_scene(np.random.default_rng(91), 3000, box=10.0)
+    big = np.argsort(s.mu_p[:, 2])[:6]          # enlarge a few Gaussians a lot
+    cov = s.cov_raw.copy()
+    cov[big, :3] += 4.0   # each covers the whole image: > 4096 entries in its round
+    from dataclasses import replace
+    s = replace(s, cov_raw=cov)
+    for size in (1024, 1040):
+        cam = scenes.orbit_camera(azimuth=0.2, elevation=0.1, distance=40.0, width=size, height=size)
+        st = raster.render_with_state(s, cam)
+        hot = raster.render(s, cam)
+        np.testing.assert_array_equal(hot, st.image)
+        imgs, cnt = raster.render_views(s, [cam, cam])
+        np.testing.assert_array_equal(imgs[0].cpu().numpy(), st.image)
+        assert int(cnt[0, 1]) == st.stats.n_entries
+    ref = oracle.render_with_state(s, scenes.orbit_camera(azimuth=0.2, elevation=0.1, distance=40.0,
+                                                          width=1024, height=1024))
+    np.testing.assert_array_equal(raster.render(s, scenes.orbit_camera(
+        azimuth=0.2, elevation=0.1, distance=40.0, width=1024, height=1024)), ref.image)
