@@ -329,14 +329,15 @@ int g6r_render(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *ca
 // Two internal streams per device for pipelining consecutive batches: a
 // batch's latency-bound projection and sort overlap the previous batch's
 // issue-bound compositing.
-static cudaStream_t g_lane[64][2];
+constexpr int kMaxLanes = 4;
+static cudaStream_t g_lane[64][kMaxLanes];
 static std::mutex g_lane_mu;
 
 static int lane_streams(cudaStream_t *out) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 1;
     std::lock_guard<std::mutex> lock(g_lane_mu);
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kMaxLanes; ++k) {
         if (!g_lane[dev][k] && cudaStreamCreateWithFlags(&g_lane[dev][k], cudaStreamNonBlocking) != cudaSuccess)
             return 1;
         out[k] = g_lane[dev][k];
@@ -362,7 +363,9 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
         const int64_t ty = (cams[0].height + cfg->tile_size - 1) / cfg->tile_size;
         per_batch = layout(scene->n, tx * ty, entry_capacity, cfg->precision).total * (size_t)nb;
     }
-    const bool piped = !prof && count > nb && per_batch && workspace_bytes >= 2 * per_batch;
+    // lanes = how many batch slices the workspace holds (2..kMaxLanes)
+    const int lanes = per_batch ? (int)std::min<size_t>(kMaxLanes, workspace_bytes / per_batch) : 1;
+    const bool piped = !prof && count > nb && lanes >= 2;
     if (!piped) {
         for (int32_t k = 0; k < count; k += nb) {
             const int nv = count - k < nb ? count - k : nb;
@@ -372,20 +375,20 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
         }
         return G6R_OK;
     }
-    cudaStream_t lane[2];
+    cudaStream_t lane[kMaxLanes];
     if (lane_streams(lane)) return cuda_check("lane streams");
-    cudaEvent_t fork, join[2];
+    cudaEvent_t fork, join[kMaxLanes];
     if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return cuda_check("event");
     cudaEventRecord(fork, st);
-    for (int l = 0; l < 2; ++l) cudaStreamWaitEvent(lane[l], fork, 0);
+    for (int l = 0; l < lanes; ++l) cudaStreamWaitEvent(lane[l], fork, 0);
     int rc = G6R_OK;
     for (int32_t k = 0, i = 0; k < count && !rc; k += nb, ++i) {
         const int nv = count - k < nb ? count - k : nb;
-        char *half = static_cast<char *>(workspace) + (size_t)(i & 1) * per_batch;
+        char *half = static_cast<char *>(workspace) + (size_t)(i % lanes) * per_batch;
         rc = render_batch(scene, group_mask, &cams[k], nv, cfg, half, per_batch, entry_capacity,
-                          &frames[k], nullptr, lane[i & 1], nullptr);
+                          &frames[k], nullptr, lane[i % lanes], nullptr);
     }
-    for (int l = 0; l < 2; ++l) {   // join (also on error, so the caller's stream stays ordered)
+    for (int l = 0; l < lanes; ++l) {   // join (also on error, so the caller's stream stays ordered)
         cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
         cudaEventRecord(join[l], lane[l]);
         cudaStreamWaitEvent(st, join[l], 0);

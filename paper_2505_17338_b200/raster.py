@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -508,6 +509,7 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
 
 DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
 MAX_BATCH = 16            # kMaxBatch in csrc/g6r_internal.h
+PIPELINE_LANES = int(os.environ.get("G6R_LANES", "2"))   # streams batches alternate over (<= 4)
 
 
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
@@ -547,8 +549,8 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     slots = max(1, min(int(concurrency), MAX_BATCH, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
-    # two batches' worth pipelines consecutive batches on two streams
-    lanes = 2 if (V > slots and profiler is None and pipeline) else 1
+    # n batches' worth of workspace pipelines consecutive batches on n streams
+    lanes = PIPELINE_LANES if (V > slots and profiler is None and pipeline) else 1
     ws = torch.empty(max(per * slots * lanes, 256), dtype=torch.uint8, device=dev)
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
     bg = (ctypes.c_double * 3)(*[float(c) for c in background])
