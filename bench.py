@@ -350,11 +350,14 @@ def run_b200(args):
         view_bytes = float(np.mean(180.0 * n + 64.0 * M + 84.0 * E + 8.0 * T + 16.0 * H * W))
         traffic = load_traffic()
         # launches per batch: clear, project, sort histogram, one onesweep per
-        # radix pass (upper bound of 9-bit passes; surplus ones exit at once),
-        # ranges, composite
-        max_passes = (32 + max(1, math.ceil(math.log2(T))) + 8) // 9
+        # radix pass (upper bound; surplus passes exit at once), composite, and
+        # either the 4 tile-partition kernels (splat-level sort, T <= 4096:
+        # depth + sentinel = 33 bits -> 4 passes) or ranges (entry sort)
         batches = math.ceil(V / max(1, min(args.concurrency, 16)))
-        launches = batches * (5 + max_passes)
+        if T <= 4096:
+            launches = batches * (4 + 4 + (33 + 8) // 9)
+        else:
+            launches = batches * (5 + (32 + max(1, math.ceil(math.log2(T))) + 8) // 9)
         line = {
             "metric": METRIC, "value": views_per_s, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / V,
