@@ -115,6 +115,19 @@ __device__ __forceinline__ unsigned long long pack_entry(unsigned long long key,
 
 __device__ __forceinline__ int pass_src(int pass) { return pass & 1; }
 
+// Lanes of the warp holding the same 10-bit value (9-bit digit or the kBins
+// "invalid" code): one ballot per bit instead of MATCH.ANY.
+__device__ __forceinline__ unsigned match_digit(unsigned d) {
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int bit = 0; bit <= kRadixBits; ++bit) {
+        const bool on = (d >> bit) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, on);
+        peers &= on ? b : ~b;
+    }
+    return peers;
+}
+
 constexpr unsigned kAgg = 1u << 30, kInc = 2u << 30, kCntMask = (1u << 30) - 1;
 constexpr int kProbe = 4;   // look-back predecessors read per round trip
 
@@ -287,7 +300,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
             const unsigned d = idx >= c.e ? (unsigned)kBins
                                : c.packed ? (unsigned)(key[k] >> (c.vbits + shift)) & (kBins - 1)
                                           : digit_of(key[k], c.dmin, c.dtop, c.dbits, shift);
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const unsigned peers = match_digit(d);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
             if (d < (unsigned)kBins && lane == leader) {
