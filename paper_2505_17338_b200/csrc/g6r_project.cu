@@ -350,7 +350,7 @@ __device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *
 // writes one depth key (f32 depth bits, all-ones for rows not drawn) and its
 // tile rect, for the splat-level sort in g6r_tiles.cu.
 template <bool kF64, bool kOrdered, bool kSplatKeys = false>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 4)
 k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_splat_out so,
           int write_entries, double sh_c0, double sh_c1) {
     __shared__ int s_tile;
@@ -380,13 +380,20 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     if (i < n) {
         const unsigned fl = scene.flags[i];
         if (((mask >> (fl & 15u)) & 1u) && !(fl & G6R_FLAG_DEGENERATE)) {
-            // all 22 column packets issued at once: one memory round trip per Gaussian
+            // two phases: the slice columns (mu_p, mu_d, adjust, precision_dd,
+            // opacity, w_norm) first, the projection columns (sigma', sh) only for
+            // splats that survive the slice -- fewer live registers, more warps
             double r[G6R_REC_DOUBLES];
 #pragma unroll
-            for (int c = 0; c < G6R_REC_COLUMNS; ++c) {
+            for (int c = 0; c < 11; ++c) {
                 const double2 q = __ldg(&rec[c * n + i]);
                 r[2 * c] = q.x;
                 r[2 * c + 1] = q.y;
+            }
+            {
+                const double2 q = __ldg(&rec[21 * n + i]);
+                r[42] = q.x;
+                r[43] = q.y;
             }
             double view[3], madj[3], quad;
             st = slice_row(r + 0, r + 3, r + 6, r + 15, vp.pos[0], vp.pos[1], vp.pos[2], view, madj,
@@ -398,7 +405,15 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
                 o.alpha = alpha;
                 if (!(alpha >= kMinAlpha)) st = 2;
             }
-            if (st == 0) st = project_row(view, madj, r + 30, r + 21, vp, sh_c0, sh_c1, o);
+            if (st == 0) {
+#pragma unroll
+                for (int c = 11; c < 21; ++c) {
+                    const double2 q = __ldg(&rec[c * n + i]);
+                    r[2 * c] = q.x;
+                    r[2 * c + 1] = q.y;
+                }
+                st = project_row(view, madj, r + 30, r + 21, vp, sh_c0, sh_c1, o);
+            }
             if (st == 0) tile_rect(o.u, o.v, o.rx, o.ry, vp, x0, y0, wx, hy);
         }
         if (so.stage) so.stage[i] = (uint8_t)st;
