@@ -78,7 +78,7 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     L.rect = o;
     o = align_up(o + (size_t)n * sizeof(uint2));
     L.chunk_hist = o;
-    o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, kChunkSplats) * tiles * sizeof(unsigned));
+    o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, chunk_splats(tiles)) * tiles * sizeof(unsigned));
     L.tile_total = o;
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.total = o;

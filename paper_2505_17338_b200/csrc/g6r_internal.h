@@ -39,6 +39,11 @@ struct Workspace {
 // expanded into tile runs by an order-preserving partition in chunks of
 // kChunkSplats sorted splats.
 constexpr int kChunkSplats = 2048;
+// chunk size by tile-grid size: larger grids use larger chunks so the per-chunk
+// work that scales with the tile count stays small per splat
+__host__ __device__ inline int chunk_splats(int64_t tiles) {
+    return tiles <= 1024 ? kChunkSplats : 4 * kChunkSplats;
+}
 constexpr int kMaxSplatSortTiles = 4096;   // larger tile grids use the entry sort
 
 struct ViewParams {

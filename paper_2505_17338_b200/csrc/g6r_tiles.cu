@@ -7,7 +7,7 @@
 // (depth, row) order".  The hot path therefore sorts the n splat rows by depth
 // once (g6r_sort.cu, splat mode: n keys instead of E entries, 8-byte items) and
 // expands them here without a second sort:
-//   k_chunk_count    per chunk of kChunkSplats sorted splats: tile histogram
+//   k_chunk_count    per chunk of chunk_splats(T) sorted splats: tile histogram
 //   k_chunk_colscan  per tile: exclusive prefix over chunks, tile totals
 //   k_tile_scan      tile_starts = exclusive scan of the totals (+ overflow)
 //   k_chunk_scatter  per chunk, in rounds of 256 splats: the round's entries
@@ -31,6 +31,7 @@ constexpr int kScatterWarps = 8;
 struct PartCtx {
     int64_t m;             // drawn splats (the first m sorted items)
     int64_t chunks;
+    int chunk;             // sorted splats per chunk
     int tiles, tiles_x;
     const unsigned long long *items;   // depth-sorted (depth code << vbits | row)
 };
@@ -40,9 +41,10 @@ __device__ __forceinline__ bool part_ctx(const Batch &b, int v, PartCtx &c) {
     const Workspace &ws = b.ws[v];
     if (cnt[G6R_CNT_OVERFLOW] || cnt[G6R_CNT_ENTRIES] > ws.entry_capacity) return false;
     c.m = cnt[G6R_CNT_DRAWN];
-    c.chunks = ceil_div(c.m, kChunkSplats);
     c.tiles_x = b.vp[v].tiles_x;
     c.tiles = b.vp[v].tiles_x * b.vp[v].tiles_y;
+    c.chunk = chunk_splats(c.tiles);
+    c.chunks = ceil_div(c.m, c.chunk);
     c.items = ws.keys[ws.internal[kSortPasses] & 1];
     return true;
 }
@@ -63,8 +65,8 @@ k_chunk_count(const __grid_constant__ Batch b, unsigned long long vmask) {
     const Workspace &ws = b.ws[v];
     for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) s_hist[t] = 0u;
     __syncthreads();
-    const int64_t s0 = (int64_t)blockIdx.x * kChunkSplats;
-    const int64_t s1 = s0 + kChunkSplats < c.m ? s0 + kChunkSplats : c.m;
+    const int64_t s0 = (int64_t)blockIdx.x * c.chunk;
+    const int64_t s1 = s0 + c.chunk < c.m ? s0 + c.chunk : c.m;
     for (int64_t sp = s0 + threadIdx.x; sp < s1; sp += blockDim.x) {
         const unsigned row = (unsigned)(c.items[sp] & vmask);
         int x0, y0, wx, hy;
@@ -197,8 +199,8 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lanemask_lt = (1u << lane) - 1u;
     unsigned *vals = ws.vals[0];
-    const int64_t c0 = (int64_t)blockIdx.x * kChunkSplats;
-    const int64_t c1 = c0 + kChunkSplats < c.m ? c0 + kChunkSplats : c.m;
+    const int64_t c0 = (int64_t)blockIdx.x * c.chunk;
+    const int64_t c1 = c0 + c.chunk < c.m ? c0 + c.chunk : c.m;
     for (int64_t r0 = c0; r0 < c1; r0 += kRound) {
         // this thread's kPerThread consecutive splats of the round
         unsigned row[kPerThread];
@@ -305,7 +307,7 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
 int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
     const int tiles = b.vp[0].tiles_x * b.vp[0].tiles_y;
-    const int64_t chunks = ceil_div(n > 0 ? n : 1, kChunkSplats);
+    const int64_t chunks = ceil_div(n > 0 ? n : 1, chunk_splats(tiles));
     const unsigned long long vmask = (1ull << vbits) - 1ull;
     const size_t count_smem = (size_t)tiles * sizeof(unsigned);
     const size_t scatter_smem =
