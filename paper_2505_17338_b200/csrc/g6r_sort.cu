@@ -22,11 +22,19 @@
 // counts, and finds its global digit offsets by decoupled look-back over the
 // earlier tiles' status words (2-bit flag | 30-bit count in one 32-bit word,
 // so a single store publishes both and no fence is needed).  The look-back
-// reads 8 predecessors per round trip.  One histogram launch before the passes
-// computes every pass's digit totals (LSD digit counts do not depend on the
-// order) and zeroes the status words.  With a batch of views per launch the
-// views' look-back chains run side by side, so the pass is bandwidth-bound
-// (24 B read+written per key) rather than bound by one chain's latency.
+// reads the immediate predecessor, then 4 per round trip.  One histogram
+// launch before the passes computes every pass's digit totals (LSD digit
+// counts do not depend on the order) and zeroes the status words.  With a
+// batch of views per launch the views' look-back chains run side by side.
+// Pass 0 packs key and value into one u64 (tile | depth code | value) when
+// they fit, so later passes move 8 bytes per item.
+//
+// Two item sets use these kernels:
+//   * entries (launch_sort): the E (tile, depth) keys of the entry path, then
+//     k_ranges;
+//   * splats (launch_splat_sort, the hot path): the n scene rows keyed by
+//     depth alone -- rows not drawn carry an all-ones key that compresses to
+//     one extra code and sorts last -- then the tile partition (g6r_tiles.cu).
 #include <algorithm>
 
 #include "g6r_common.cuh"
