@@ -259,6 +259,28 @@ def test_determinism_repeat_and_concurrent():
         np.testing.assert_array_equal(o, base)
 
 
+def test_concurrent_pipelined_batches_from_threads():
+    """Several host threads render pipelined multi-batch calls on their own
+    streams at once (the library's internal lane streams are shared): every
+    result equals the single-threaded one."""
+    import torch
+    s = scenes.random_scene(np.random.default_rng(62), 20000)
+    cams = scenes.orbit_ring(s, count=20, size=96)
+    base = raster.render_batch(s, cams)
+    out = [None] * 4
+
+    def work(i):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            imgs, _ = raster.render_views(s, cams)
+            out[i] = imgs.cpu().numpy()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for o in out:
+        np.testing.assert_array_equal(o, base)
+
+
 def test_degenerate_policy_on_device():
     s = scenes.random_scene(np.random.default_rng(83), 300)
     cov = s.cov_raw.copy()
