@@ -10,13 +10,12 @@
 //   k_chunk_count    per chunk of chunk_splats(T) sorted splats: tile histogram
 //   k_chunk_colscan  per tile: exclusive prefix over chunks, tile totals
 //   k_tile_scan      tile_starts = exclusive scan of the totals (+ overflow)
-//   k_chunk_scatter  per chunk, in rounds of 256 splats: the round's entries
-//                    are expanded in order into a shared window, each warp
-//                    ranks a contiguous slice of the window with match-any on
-//                    the tile id and 16-bit per-warp counters, the counters are
-//                    prefixed over warps, and every entry's splat row is
-//                    written to tile_start + chunk prefix + running count +
-//                    warp prefix + rank.
+//   k_chunk_scatter  per chunk: each warp recounts its slice of the chunk per
+//                    tile, the counts are prefixed over warps, then each warp
+//                    expands its splats' entries in order and ranks them with
+//                    match-any on the tile id against its running counters;
+//                    every entry's splat row is written to tile_start + chunk
+//                    prefix + warp prefix + running count + rank.
 // Every step is deterministic and keeps the sorted order, so runs, tile starts
 // and images are bit-identical to the entry sort's.
 #include <algorithm>
@@ -54,6 +53,56 @@ __device__ __forceinline__ void unpack_rect(uint2 r, int &x0, int &y0, int &wx, 
     y0 = (int)(r.x >> 16);
     wx = (int)(r.y & 0xffffu);
     hy = (int)(r.y >> 16);
+}
+
+// Load-balanced entry enumeration for a warp's group of 32 sorted splats.
+// Lane i holds splat i's row, packed rect and its inclusive/exclusive entry
+// prefix over the group; entry s (0 <= s < total, row-major within each rect,
+// rects in lane order) is owned by the first lane whose inclusive prefix
+// exceeds s, found by a 5-step shuffle search.  Every lane then decodes one
+// entry, so a group costs the same whatever the spread of rect sizes.
+struct EntryGroup {
+    unsigned row, rx, ry;   // splat row, packed (x0 | y0 << 16), (wx | hy << 16)
+    int excl, incl, total;
+};
+
+__device__ __forceinline__ EntryGroup load_group(const PartCtx &c, const Workspace &ws, int64_t sp,
+                                                 int64_t end, unsigned long long vmask) {
+    EntryGroup g;
+    g.row = 0;
+    g.rx = 0;
+    g.ry = 0;
+    if (sp < end) {
+        g.row = (unsigned)(c.items[sp] & vmask);
+        const uint2 r = ws.rect[g.row];
+        g.rx = r.x;
+        g.ry = r.y;
+    }
+    const int cnt = (int)((g.ry & 0xffffu) * (g.ry >> 16));
+    g.incl = warp_inclusive_scan(cnt);
+    g.excl = g.incl - cnt;
+    g.total = __shfl_sync(0xffffffffu, g.incl, 31);
+    return g;
+}
+
+// tile of entry s of the group (any value for s >= total); row of its splat
+__device__ __forceinline__ unsigned group_entry(const EntryGroup &g, int s, int tiles_x, unsigned &row) {
+    int L = 0;
+#pragma unroll
+    for (int b = 16; b; b >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, g.incl, L + b - 1);
+        if (v <= s) L += b;
+    }
+    const int k = s - __shfl_sync(0xffffffffu, g.excl, L);
+    const unsigned a = __shfl_sync(0xffffffffu, g.rx, L);
+    const unsigned w = __shfl_sync(0xffffffffu, g.ry, L);
+    row = __shfl_sync(0xffffffffu, g.row, L);
+    const int wx = (int)(w & 0xffffu);
+    // k / wx: k < wx * hy <= 4096 entries, so the float quotient is never
+    // within an ulp of the next integer
+    const int qy = (int)__fdividef((float)k + 0.5f, (float)wx);
+    const int qx = k - qy * wx;
+    return (unsigned)(((int)(a >> 16) + qy) * tiles_x + (int)(a & 0xffffu) + qx);
 }
 
 __global__ void __launch_bounds__(kBlock)
@@ -170,138 +219,87 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const __grid_constant__ Batc
     }
 }
 
-constexpr int kPerThread = 4;                 // sorted splats per thread per round
-constexpr int kRound = kBlock * kPerThread;   // 1024 splats per round
-constexpr int kWindow = 4096;                 // expanded entries ranked at a time
-constexpr int kWinPerWarp = kWindow / kScatterWarps;   // 512: 16 groups of 32
-constexpr int kGroups = kWinPerWarp / 32;
-constexpr size_t kScatterStatic = (size_t)kWindow * (2 * sizeof(unsigned) + sizeof(unsigned short));
-
+// k_chunk_scatter: CTA = chunk, warp w owns the w-th eighth of the chunk's
+// sorted splats.  Pass 1: each warp counts its entries per tile (16-bit
+// counters, two per shared word, bumped with 32-bit shared atomics; a chunk
+// puts at most chunk_splats(T) <= 8192 entries in one tile, so halves never
+// carry).  The counters are then prefixed over warps in place (the packed
+// words add lane-wise for the same reason) and tile_start + chunk prefix is
+// kept per tile.  Pass 2: each warp walks its splats again in groups of 32,
+// enumerates the group's entries in order 32 at a time (group_entry) and ranks
+// them with match-any on the tile id against its own running counters; the
+// leader of each tile's peers advances the counter.  No CTA
+// barrier inside either pass, and every position is a function of the sorted
+// order alone.
 __global__ void __launch_bounds__(kBlock)
 k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     extern __shared__ __align__(16) unsigned char s_raw[];
-    __shared__ unsigned s_wsum[kScatterWarps];
     const int v = blockIdx.y;
     PartCtx c;
     if (!part_ctx(b, v, c) || blockIdx.x >= c.chunks) return;
     const Workspace &ws = b.ws[v];
-    // dynamic shared memory: window (tile, row, rank), then per-tile state
-    unsigned *s_ewin = reinterpret_cast<unsigned *>(s_raw);                    // [kWindow]
-    unsigned *s_rwin = s_ewin + kWindow;                                       // [kWindow]
-    unsigned short *s_rank = reinterpret_cast<unsigned short *>(s_rwin + kWindow);   // [kWindow]
-    unsigned *s_base = reinterpret_cast<unsigned *>(s_rank + kWindow);         // [T]
-    unsigned short *s_cnt = reinterpret_cast<unsigned short *>(s_base + c.tiles);   // [warps][T]
-    unsigned short *s_tot = s_cnt + kScatterWarps * c.tiles;                        // [T]
-    const unsigned *chunk_off = ws.chunk_hist + (int64_t)blockIdx.x * c.tiles;
-    for (int t = threadIdx.x; t < c.tiles; t += blockDim.x)
-        s_base[t] = (unsigned)ws.tile_starts[t] + chunk_off[t];
-    for (int k = threadIdx.x; k < kScatterWarps * c.tiles; k += blockDim.x) s_cnt[k] = 0;
+    const int T = c.tiles;
+    const int tw = (T + 1) >> 1;   // packed counter words per warp
+    unsigned *s_tb = reinterpret_cast<unsigned *>(s_raw);                  // [T] tile start + chunk prefix
+    unsigned *s_cw = s_tb + T;                                              // [warps][tw] packed u16 counters
+    const unsigned *chunk_off = ws.chunk_hist + (int64_t)blockIdx.x * T;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) s_tb[t] = (unsigned)ws.tile_starts[t] + chunk_off[t];
+    for (int k = threadIdx.x; k < kScatterWarps * tw; k += blockDim.x) s_cw[k] = 0u;
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lanemask_lt = (1u << lane) - 1u;
-    unsigned *vals = ws.vals[0];
+    const int per = c.chunk / kScatterWarps;
     const int64_t c0 = (int64_t)blockIdx.x * c.chunk;
-    const int64_t c1 = c0 + c.chunk < c.m ? c0 + c.chunk : c.m;
-    for (int64_t r0 = c0; r0 < c1; r0 += kRound) {
-        // this thread's kPerThread consecutive splats of the round
-        unsigned row[kPerThread];
-        uint2 rc[kPerThread];
-        int cnt_all = 0;
-#pragma unroll
-        for (int q = 0; q < kPerThread; ++q) {
-            const int64_t sp = r0 + threadIdx.x * kPerThread + q;
-            row[q] = sp < c1 ? (unsigned)(c.items[sp] & vmask) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kPerThread; ++q) {
-            const int64_t sp = r0 + threadIdx.x * kPerThread + q;
-            rc[q] = sp < c1 ? ws.rect[row[q]] : make_uint2(0u, 0u);
-            cnt_all += (int)((rc[q].y & 0xffffu) * (rc[q].y >> 16));
-        }
-        const int inc = warp_inclusive_scan(cnt_all);
-        __syncthreads();   // previous round's window and s_wsum are free
-        if (lane == 31) s_wsum[warp] = (unsigned)inc;
-        __syncthreads();
-        int pre = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kScatterWarps; ++w) {
-            const int x = (int)s_wsum[w];
-            pre += w < warp ? x : 0;
-            total += x;
-        }
-        const int off0 = pre + inc - cnt_all;   // first entry of this thread's splats
-        for (int w0 = 0; w0 < total; w0 += kWindow) {
-            const int wn = total - w0 < kWindow ? total - w0 : kWindow;
-            // expand this thread's entries inside [w0, w0 + wn), in order
-            int off = off0;
-#pragma unroll
-            for (int q = 0; q < kPerThread; ++q) {
-                int x0, y0, wx, hy;
-                unpack_rect(rc[q], x0, y0, wx, hy);
-                const int cnt = wx * hy;
-                const int k_lo = w0 > off ? w0 - off : 0;
-                const int k_hi = off + cnt < w0 + wn ? cnt : w0 + wn - off;
-                if (k_lo < k_hi) {   // row-major walk of the rect from entry k_lo
-                    int qy = k_lo / wx, qx = k_lo - qy * wx;
-                    unsigned t = (unsigned)((y0 + qy) * c.tiles_x + x0 + qx);
-                    for (int k = k_lo; k < k_hi; ++k) {
-                        s_ewin[off + k - w0] = t;
-                        s_rwin[off + k - w0] = row[q];
-                        if (++qx == wx) {
-                            qx = 0;
-                            t += (unsigned)(c.tiles_x - wx + 1);
-                        } else {
-                            ++t;
-                        }
-                    }
-                }
-                off += cnt;
-            }
-            __syncthreads();
-            // rank: warp w owns window slots [w*512, w*512+512), 32 at a time in order
-#pragma unroll 4
-            for (int g = 0; g < kGroups; ++g) {
-                const int slot = warp * kWinPerWarp + g * 32 + lane;
-                const bool valid = slot < wn;
-                const unsigned t = valid ? s_ewin[slot] : 0xffffffffu;
-                const unsigned peers = __match_any_sync(0xffffffffu, t);
-                const int leader = __ffs(peers) - 1;
-                unsigned old = 0;
-                if (valid && lane == leader) {
-                    old = s_cnt[warp * c.tiles + t];
-                    s_cnt[warp * c.tiles + t] = (unsigned short)(old + (unsigned)__popc(peers));
-                }
-                old = __shfl_sync(0xffffffffu, old, leader);
-                if (valid) s_rank[slot] = (unsigned short)(old + (unsigned)__popc(peers & lanemask_lt));
-                __syncwarp();
-            }
-            __syncthreads();
-            // per tile: the warp counts become exclusive offsets (warps in order)
-            for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) {
-                unsigned run = 0;
-#pragma unroll
-                for (int w = 0; w < kScatterWarps; ++w) {
-                    const unsigned x = s_cnt[w * c.tiles + t];
-                    s_cnt[w * c.tiles + t] = (unsigned short)run;
-                    run += x;
-                }
-                s_tot[t] = (unsigned short)run;
-            }
-            __syncthreads();
-            // scatter: tile base + warp offset + rank
-            for (int slot = threadIdx.x; slot < wn; slot += blockDim.x) {
-                const unsigned t = s_ewin[slot];
-                vals[s_base[t] + s_cnt[(slot / kWinPerWarp) * c.tiles + t] + s_rank[slot]] = s_rwin[slot];
-            }
-            __syncthreads();
-            // advance the bases by this window's counts and clear the counters
-            for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) {
-                s_base[t] += s_tot[t];
-#pragma unroll
-                for (int w = 0; w < kScatterWarps; ++w) s_cnt[w * c.tiles + t] = 0;
-            }
-            __syncthreads();
+    const int64_t chunk_end = c0 + c.chunk < c.m ? c0 + c.chunk : c.m;
+    const int64_t w0s = c0 + (int64_t)warp * per;
+    const int64_t w1s = w0s + per < chunk_end ? w0s + per : chunk_end;
+    unsigned *cw = s_cw + warp * tw;
+    unsigned short *cnt16 = reinterpret_cast<unsigned short *>(cw);
+    // pass 1: this warp's entries per tile
+    for (int64_t g0 = w0s; g0 < w1s; g0 += 32) {
+        const EntryGroup g = load_group(c, ws, g0 + lane, w1s, vmask);
+        for (int q0 = 0; q0 < g.total; q0 += 32) {
+            unsigned row;
+            const unsigned t = group_entry(g, q0 + lane, c.tiles_x, row);
+            if (q0 + lane < g.total) atomicAdd(&cw[t >> 1], 1u << ((t & 1u) * 16u));
         }
     }
+    __syncthreads();
+    // exclusive prefix of the per-warp counts, per tile (packed pairs)
+    for (int k = threadIdx.x; k < tw; k += blockDim.x) {
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kScatterWarps; ++w) {
+            const unsigned x = s_cw[w * tw + k];
+            s_cw[w * tw + k] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    // pass 2: rank and scatter, 32 entries at a time
+    unsigned *vals = ws.vals[0];
+    for (int64_t g0 = w0s; g0 < w1s; g0 += 32) {
+        const EntryGroup g = load_group(c, ws, g0 + lane, w1s, vmask);
+        for (int q0 = 0; q0 < g.total; q0 += 32) {
+            const bool valid = q0 + lane < g.total;
+            unsigned row;
+            unsigned t = group_entry(g, q0 + lane, c.tiles_x, row);
+            t = valid ? t : 0xffffffffu;
+            const unsigned peers = __match_any_sync(0xffffffffu, t);
+            const int leader = __ffs(peers) - 1;
+            unsigned old = 0;
+            if (valid && lane == leader) {
+                old = cnt16[t];
+                cnt16[t] = (unsigned short)(old + (unsigned)__popc(peers));
+            }
+            old = __shfl_sync(0xffffffffu, old, leader);
+            if (valid) vals[s_tb[t] + old + (unsigned)__popc(peers & lanemask_lt)] = row;
+        }
+    }
+}
+
+static size_t scatter_smem_bytes(int tiles) {
+    return (size_t)tiles * sizeof(unsigned) + (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
 }
 
 int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st) {
@@ -310,14 +308,13 @@ int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st)
     const int64_t chunks = ceil_div(n > 0 ? n : 1, chunk_splats(tiles));
     const unsigned long long vmask = (1ull << vbits) - 1ull;
     const size_t count_smem = (size_t)tiles * sizeof(unsigned);
-    const size_t scatter_smem =
-        kScatterStatic + (size_t)tiles * (sizeof(unsigned) + (kScatterWarps + 1) * sizeof(unsigned short));
+    const size_t scatter_smem = scatter_smem_bytes(tiles);
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(k_chunk_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kMaxSplatSortTiles * sizeof(unsigned)));
         cudaFuncSetAttribute(k_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kScatterStatic + kMaxSplatSortTiles * (sizeof(unsigned) + (kScatterWarps + 1) * sizeof(unsigned short))));
+                             (int)scatter_smem_bytes(kMaxSplatSortTiles));
         attrs = true;
     }
     const dim3 cgrid((unsigned)chunks, (unsigned)b.nviews);
