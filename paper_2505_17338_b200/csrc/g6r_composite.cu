@@ -147,8 +147,15 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
     return r;
 }
 __device__ __forceinline__ ExpOperands exp_operands(uint32_t tab) { return ExpOperands{opaque(tab)}; }
+__device__ __forceinline__ uint2 lds_u32x2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
 
-// glibc expf (g6r_common.cuh expf_glibc, same operations) with the operands above
+// glibc expf (g6r_common.cuh expf_glibc, same operations) with the operands
+// above.  The scale 2^(k/32) is the table entry with k's low 17 bits added to
+// its exponent field: (k << 47) only touches the high word, so one 32-bit add.
 __device__ __forceinline__ float splat_exp_s(float x, const ExpOperands &e) {
     const double kInvLn2N = c_exp_k[0];
     const double kShift = 0x1.8p+52;
@@ -157,11 +164,11 @@ __device__ __forceinline__ float splat_exp_s(float x, const ExpOperands &e) {
     const double xd = (double)x;
     const double z = __dmul_rn(kInvLn2N, xd);
     double kd = __dadd_rn(z, kShift);
-    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    const unsigned ki = (unsigned)__double2loint(kd);
     kd = __dsub_rn(kd, kShift);
     const double r = __fma_rn(kInvLn2N, xd, -kd);
-    const unsigned long long t = lds_u64(tab + 8u * (unsigned)(ki & 31ull)) + (ki << 47);
-    const double s = __longlong_as_double((long long)t);
+    const uint2 t = lds_u32x2(tab + 8u * (ki & 31u));
+    const double s = __hiloint2double((int)(t.y + (ki << 15)), (int)t.x);
     const double p = __fma_rn(c0, r, c1);
     const double r2 = __dmul_rn(r, r);
     double y = __fma_rn(c2, r, 1.0);
@@ -251,9 +258,10 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     const Real fx = (Real)px, fy = (Real)py;
     const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
     const Real half = (Real)-0.5, one = (Real)1;
-    Real T = one, ar = 0, ag = 0, ab = 0, aa = 0;
+    // a pixel is finished once T < t_stop (T never grows); pixels outside the
+    // image start finished
+    Real T = inside ? one : (Real)0, ar = 0, ag = 0, ab = 0, aa = 0;
     int last = 0;
-    bool done = !inside;
     __syncthreads();   // s_wbox / s_tab ready
 
     // stage batch k's entry (this thread's) into buffer `buf`
@@ -285,7 +293,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         const uint32_t bsp = sp_base + (uint32_t)(buf * nb) * (uint32_t)sizeof(S);
         const uint32_t bmask = mask_base + (uint32_t)(buf * nb) * 4u;
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
-        if (!__all_sync(wmask, done)) {
+        if (!__all_sync(wmask, T < t_stop)) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
                 unsigned hits = 0;   // splats c0..c0+31 that can touch this warp
                 for (int k = 0; k < 32; k += wlanes) {
@@ -297,7 +305,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                 while (hits) {
                     const int j = c0 + __ffs(hits) - 1;
                     hits &= hits - 1;
-                    if (done) continue;
+                    if (T < t_stop) continue;
                     S s;
                     lds_splat(bsp + (uint32_t)j * (uint32_t)sizeof(S), s);
                     Real mx, my, ca, cb, cc, al;
@@ -317,14 +325,13 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                     aa = aa + w;
                     T = T * (one - ai);
                     last = (int)(b0 - lo) + j + 1;
-                    if (T < t_stop) done = true;
                 }
             }
         }
         // the other buffer was last read in the previous batch (fenced by the
         // barrier that ended it), so the prefetched splat can land there now
         stage(b0 + nb, buf ^ 1, pre, have1);
-        if (__syncthreads_count(!done) == 0) break;
+        if (__syncthreads_count(!(T < t_stop)) == 0) break;
     }
     if (inside) {
         const int64_t p = (int64_t)py * vp.iw + px;
