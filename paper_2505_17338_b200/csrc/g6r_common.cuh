@@ -106,9 +106,23 @@ __device__ __forceinline__ void cull_extents(double a, double b, double c, doubl
     ey = (float)(k * sqrt(a / det) * grow + 1e-3);
 }
 
+// Same bound for the f32 compositor, in float with the SFU approximations
+// (lg2, rcp, rsqrt; a few ulp each, far inside the 1e-4 / 1e-3 margins).  The
+// compositor's alpha is al * expf(pw) <= al, so al < (float)(1/255) can never
+// pass its floor; a NaN al would pass it wherever the power is in range.
+__device__ __forceinline__ float cull_q_f32(float alpha) {
+    const float floor_f = (float)(1.0 / 255.0);   // the compositor's floor_a
+    if (alpha < floor_f) return -1.0f;
+    if (!(alpha == alpha)) return 9.0f;
+    // ln(alpha / floor_f) <= ln(255 alpha) since floor_f > 1/255
+    const float qa = 2.0f * __logf(alpha * 255.0f) * (1.0f + 1e-4f) + 1e-3f;
+    return qa < 9.0f ? qa : 9.0f;
+}
+
 // Same extents for an f32 conic, in float arithmetic (the determinant exactly
-// from the f32 products in double).  The float evaluation adds at most a few
-// ulp (~1e-6 relative); the extra 1e-5 relative growth absorbs it.
+// from the f32 products in double).  The float evaluation with approximate
+// reciprocal / square roots adds at most a few ulp (~1e-6 relative); the
+// extra 1e-5 relative growth absorbs it.
 __device__ __forceinline__ void cull_extents_f32(float a, float b, float c, float &ex, float &ey,
                                                  float alpha = 1.0f) {
     const double detd = (double)a * (double)c - (double)b * (double)b;
@@ -117,22 +131,23 @@ __device__ __forceinline__ void cull_extents_f32(float a, float b, float c, floa
         ex = ey = inf;
         return;
     }
-    const float inv = 1.0f / (float)detd;
+    const float inv = __fdividef(1.0f, (float)detd);
     const float kappa = (a + c) * (a + c) * 0.25f * inv;
     const float delta = 64.0f * 0x1p-23f * kappa + 1e-5f;
     if (!(delta < 0.5f)) {
         ex = ey = inf;
         return;
     }
-    const double q = cull_q((double)alpha);
-    if (q < 0.0) {
+    const float q = cull_q_f32(alpha);
+    if (q < 0.0f) {
         ex = ey = __int_as_float(0x7fffffff);
         return;
     }
     const float grow = 1.0f + delta;
-    const float k = (float)sqrt(q) * (1.0f + 1e-6f);
-    ex = k * sqrtf(c * inv) * grow + 1e-3f;
-    ey = k * sqrtf(a * inv) * grow + 1e-3f;
+    const float k = q * rsqrtf(q) * (1.0f + 1e-6f);
+    const float xc = c * inv, xa = a * inv;
+    ex = k * (xc * rsqrtf(xc)) * grow + 1e-3f;
+    ey = k * (xa * rsqrtf(xa)) * grow + 1e-3f;
 }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -360,6 +360,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     __shared__ EmitSmem es;
     __shared__ unsigned s_dext[2];   // block max of ~depth_bits and of depth_bits
     __shared__ int s_nbig;
+    __shared__ unsigned s_tot[2];   // splat-keys mode: drawn splats, entries
     const int v = blockIdx.x;
     const ViewParams &vp = b.vp[v];
     const Workspace &ws = b.ws[v];
@@ -368,6 +369,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     if (threadIdx.x < 6) s_fate[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_dext[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_nbig = 0;
+    if (threadIdx.x < 2) s_tot[threadIdx.x] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t n = scene.n;
@@ -423,18 +425,29 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     const int cnt = kept ? wx * hy : 0;
     const unsigned db = kept ? __float_as_uint((float)o.depth) : 0u;
     depth_extrema(kept, db, s_dext);
-    int lm, le, bm, be;
-    block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
-    if (kOrdered) {
-        lookback2(tile, bm, be, ws, &s_pm, &s_pe);
-    } else if (threadIdx.x == 0) {   // reserve this CTA's entry block; count its splats
-        s_pm = 0;
-        s_pe = (long long)atomicAdd((unsigned long long *)&counters[G6R_CNT_ENTRIES],
-                                    (unsigned long long)be);
-        if (bm) atomicAdd((unsigned long long *)&counters[G6R_CNT_DRAWN], (unsigned long long)bm);
+    int lm = 0, le = 0, bm = 0, be = 0;
+    long long m_base = 0, e_base = 0;
+    if (kSplatKeys) {   // only the CTA totals are needed (no entry block)
+        const int wm = __reduce_add_sync(0xffffffffu, kept);
+        const int we = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0 && wm) {
+            atomicAdd(&s_tot[0], (unsigned)wm);
+            atomicAdd(&s_tot[1], (unsigned)we);
+        }
+    } else {
+        block_scan2(kept, cnt, lm, le, s_wa, s_wb, bm, be);
+        if (kOrdered) {
+            lookback2(tile, bm, be, ws, &s_pm, &s_pe);
+        } else if (threadIdx.x == 0) {   // reserve this CTA's entry block; count its splats
+            s_pm = 0;
+            s_pe = (long long)atomicAdd((unsigned long long *)&counters[G6R_CNT_ENTRIES],
+                                        (unsigned long long)be);
+            if (bm) atomicAdd((unsigned long long *)&counters[G6R_CNT_DRAWN], (unsigned long long)bm);
+        }
+        __syncthreads();
+        m_base = s_pm;
+        e_base = s_pe;
     }
-    __syncthreads();
-    const long long m_base = s_pm, e_base = s_pe;
     if (kept) {
         const long long m = kOrdered ? m_base + lm : i;
         if (kF64) {
@@ -492,6 +505,10 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
                               : make_uint2(0u, 0u);
         }
         __syncthreads();
+        if (threadIdx.x == 0 && s_tot[0]) {
+            atomicAdd((unsigned long long *)&counters[G6R_CNT_DRAWN], (unsigned long long)s_tot[0]);
+            atomicAdd((unsigned long long *)&counters[G6R_CNT_ENTRIES], (unsigned long long)s_tot[1]);
+        }
         if (threadIdx.x < 6 && s_fate[threadIdx.x])
             atomicAdd((unsigned long long *)&counters[G6R_CNT_FATE + threadIdx.x],
                       (unsigned long long)s_fate[threadIdx.x]);
