@@ -420,7 +420,10 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
         }
         if (so.stage) so.stage[i] = (uint8_t)st;
     }
-    if (st < 6) atomicAdd(&s_fate[st], 1u);
+    {   // fate histogram: one shared atomic per distinct fate in the warp
+        const unsigned peers = __match_any_sync(0xffffffffu, st);
+        if (st < 6 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_fate[st], (unsigned)__popc(peers));
+    }
     const int kept = st == 0;
     const int cnt = kept ? wx * hy : 0;
     const unsigned db = kept ? __float_as_uint((float)o.depth) : 0u;
