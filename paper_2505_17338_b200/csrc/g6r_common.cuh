@@ -119,6 +119,19 @@ __device__ __forceinline__ float cull_q_f32(float alpha) {
     return qa < 9.0f ? qa : 9.0f;
 }
 
+// Lowest power at which a splat of peak alpha `alpha` can still pass the
+// compositor's alpha floor: -q/2 for the (margined) cull_q bound, never below
+// the -4.5 cutoff.  Below it alpha * expf(power) < 1/255 in the compositor's
+// own rounding, so skipping those pixels before the expf changes no bit.
+__device__ __forceinline__ float power_floor_f32(float alpha) {
+    const float q = cull_q_f32(alpha);
+    return q >= 0.0f ? fmaxf(-0.5f * q, -4.5f) : -4.5f;
+}
+__device__ __forceinline__ double power_floor(double alpha) {
+    const double q = cull_q(alpha);
+    return q >= 0.0 ? fmax(-0.5 * q, -4.5) : -4.5;
+}
+
 // Same extents for an f32 conic, in float arithmetic (the determinant exactly
 // from the f32 products in double).  The float evaluation with approximate
 // reciprocal / square roots adds at most a few ulp (~1e-6 relative); the

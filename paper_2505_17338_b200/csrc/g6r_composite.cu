@@ -31,7 +31,7 @@ struct Px<float> {
     struct alignas(16) S {
         float4 a;   // mx, my, conic a, conic b
         float4 b;   // conic c, alpha, r, g
-        float c;    // b
+        float2 c;   // b, power floor
     };
     __device__ static S unpack(const Payload &p, float &ex, float &ey) {
         ex = p.c.y;
@@ -39,7 +39,7 @@ struct Px<float> {
         S s;
         s.a = p.a;
         s.b = p.b;
-        s.c = p.c.x;
+        s.c = make_float2(p.c.x, p.c.w);
         return s;
     }
     __device__ static float mx(const S &s) { return s.a.x; }
@@ -50,7 +50,7 @@ struct Px<double> {
     using Payload = PayloadF64;
     struct alignas(16) S {
         double2 a, b, c, d;   // (mx,my) (ca,cb) (cc,alpha) (r,g)
-        double e;             // b
+        double2 e;            // (b, power floor)
     };
     __device__ static S unpack(const Payload &p, float &ex, float &ey) {
         ex = (float)p.e.y;
@@ -60,7 +60,7 @@ struct Px<double> {
         s.b = p.b;
         s.c = p.c;
         s.d = p.d;
-        s.e = p.e.x;
+        s.e = make_double2(p.e.x, p.f.y);
         return s;
     }
     __device__ static double mx(const S &s) { return s.a.x; }
@@ -73,15 +73,17 @@ __device__ __forceinline__ void fields(const Px<float>::S &s, float &mx, float &
     mx = s.a.x; my = s.a.y; ca = s.a.z; cb = s.a.w; cc = s.b.x; al = s.b.y;
 }
 __device__ __forceinline__ void colours(const Px<float>::S &s, float &r, float &g, float &b) {
-    r = s.b.z; g = s.b.w; b = s.c;
+    r = s.b.z; g = s.b.w; b = s.c.x;
 }
+__device__ __forceinline__ float power_lo(const Px<float>::S &s) { return s.c.y; }
 __device__ __forceinline__ void fields(const Px<double>::S &s, double &mx, double &my, double &ca,
                                        double &cb, double &cc, double &al) {
     mx = s.a.x; my = s.a.y; ca = s.b.x; cb = s.b.y; cc = s.c.x; al = s.c.y;
 }
 __device__ __forceinline__ void colours(const Px<double>::S &s, double &r, double &g, double &b) {
-    r = s.d.x; g = s.d.y; b = s.e;
+    r = s.d.x; g = s.d.y; b = s.e.x;
 }
+__device__ __forceinline__ double power_lo(const Px<double>::S &s) { return s.e.y; }
 
 // Pixel of thread t in a tile: 16x16 tiles give each warp an 8x4 block (so the
 // per-warp culling box is square-ish); other tile sizes are row-major.
@@ -112,14 +114,14 @@ __device__ __forceinline__ void lds_splat(uint32_t a, Px<float>::S &s) {
                  : "=f"(s.a.x), "=f"(s.a.y), "=f"(s.a.z), "=f"(s.a.w) : "r"(a));
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];"
                  : "=f"(s.b.x), "=f"(s.b.y), "=f"(s.b.z), "=f"(s.b.w) : "r"(a));
-    asm volatile("ld.shared.f32 %0, [%1+32];" : "=f"(s.c) : "r"(a));
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+32];" : "=f"(s.c.x), "=f"(s.c.y) : "r"(a));
 }
 __device__ __forceinline__ void lds_splat(uint32_t a, Px<double>::S &s) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s.a.x), "=d"(s.a.y) : "r"(a));
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(s.b.x), "=d"(s.b.y) : "r"(a));
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+32];" : "=d"(s.c.x), "=d"(s.c.y) : "r"(a));
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+48];" : "=d"(s.d.x), "=d"(s.d.y) : "r"(a));
-    asm volatile("ld.shared.f64 %0, [%1+64];" : "=d"(s.e) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+64];" : "=d"(s.e.x), "=d"(s.e.y) : "r"(a));
 }
 __device__ __forceinline__ unsigned lds_u32(uint32_t a) {
     unsigned v;
@@ -256,7 +258,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     const unsigned *__restrict__ vals = wsv.vals[sorted ? sorted_buffer(wsv.internal) : 0];
     const int64_t lo = starts[tile], hi = starts[tile + 1];
     const Real fx = (Real)px, fy = (Real)py;
-    const Real skip_lo = (Real)-4.5, floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
+    const Real floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
     const Real half = (Real)-0.5, one = (Real)1;
     // a pixel is finished once T < t_stop (T never grows); pixels outside the
     // image start finished
@@ -313,7 +315,9 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                     const Real dx = fx - mx;
                     const Real dy = fy - my;
                     const Real pw = half * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
-                    if (pw > (Real)0 || pw < skip_lo) continue;
+                    // power_lo >= -4.5: below it the alpha floor rejects the
+                    // pixel anyway, so the expf is skipped, no bit changes
+                    if (pw > (Real)0 || pw < power_lo(s)) continue;
                     const Real ai = al * splat_exp_s(pw, eops);
                     if (ai < floor_a) continue;
                     Real r, g, b;
@@ -372,7 +376,7 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
         PayloadF32 p;
         p.a = make_float4(means2d[2 * i], means2d[2 * i + 1], conics[3 * i], conics[3 * i + 1]);
         p.b = make_float4(conics[3 * i + 2], alphas[i], colors[3 * i], colors[3 * i + 1]);
-        p.c = make_float4(colors[3 * i + 2], ex, ey, 0.f);
+        p.c = make_float4(colors[3 * i + 2], ex, ey, power_floor_f32((float)alphas[i]));
         out[i] = p;
     } else {
         PayloadF64 p;
@@ -381,7 +385,7 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
         p.c = make_double2(conics[3 * i + 2], alphas[i]);
         p.d = make_double2(colors[3 * i], colors[3 * i + 1]);
         p.e = make_double2(colors[3 * i + 2], (double)ex);
-        p.f = make_double2((double)ey, 0.0);
+        p.f = make_double2((double)ey, power_floor((double)alphas[i]));
         out[i] = p;
     }
 }

@@ -462,7 +462,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             p.c = make_double2(o.cc, o.alpha);
             p.d = make_double2(o.r, o.g);
             p.e = make_double2(o.b, (double)ex);
-            p.f = make_double2((double)ey, 0.0);
+            p.f = make_double2((double)ey, power_floor(o.alpha));
             reinterpret_cast<PayloadF64 *>(ws.payload)[m] = p;
         } else {
             const float fa = (float)o.ca, fb = (float)o.cb, fc = (float)o.cc;
@@ -472,7 +472,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             PayloadF32 p;
             p.a = make_float4((float)o.u, (float)o.v, fa, fb);
             p.b = make_float4(fc, fal, (float)o.r, (float)o.g);
-            p.c = make_float4((float)o.b, ex, ey, 0.f);
+            p.c = make_float4((float)o.b, ex, ey, power_floor_f32(fal));
             reinterpret_cast<PayloadF32 *>(ws.payload)[m] = p;
         }
         if (kOrdered) {
