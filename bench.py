@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--batch", "--concurrency", dest="concurrency", type=int, default=8,
                     help="views per kernel launch (1..8; 1 = one view at a time)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exp", choices=("fast", "exact"), default="fast",
+                    help="f32 compositor exp: SFU ex2 (image within the 1e-3 / 60 dB parity "
+                         "bound) or glibc expf restated (framebuffer bit-identical)")
     return ap.parse_args()
 
 
@@ -246,7 +249,8 @@ def run_b200(args):
     else:
         scene = host_scene
     n = len(scene)
-    cfg = RenderConfig()
+    cfg = RenderConfig(exp_mode=args.exp)
+    other = RenderConfig(exp_mode="exact" if args.exp == "fast" else "fast")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     prep = raster.prepare_scene(scene)
@@ -297,6 +301,28 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     elapsed = ev0.elapsed_time(ev1)
+    # the other exp mode, same views and timing (reported beside the headline),
+    # and how far the two framebuffers are apart on the first batch
+    raster.render_views(scene, cams, config=other, capacity=cap, out=images,
+                        concurrency=args.concurrency)   # warm-up
+    torch.cuda.synchronize()
+    ev0.record()
+    raster.render_views(scene, cams, config=other, capacity=cap, out=images,
+                        concurrency=args.concurrency)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_other = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_other, op=dist.ReduceOp.MAX)
+    k0 = min(8, len(cams))
+    img_a = raster.render_views(scene, cams[:k0], config=cfg, capacity=cap)[0]
+    img_b = raster.render_views(scene, cams[:k0], config=other, capacity=cap)[0]
+    d = (img_a[..., :3].double() - img_b[..., :3].double())
+    mse = (d * d).flatten(1).mean(1).clamp_min(1e-30)
+    mode_diff = {"views": k0, "max_abs": float(d.abs().max().item()),
+                 "min_psnr_db": float((10.0 * torch.log10(1.0 / mse)).min().item()),
+                 "bitwise_equal_pixels": float((img_a == img_b).all(-1).double().mean().item())}
+    del img_a, img_b, d
     # stage split: the same views again (untimed) with per-batch stage events,
     # which keeps the batches on one stream
     raster.render_views(scene, cams, config=cfg, capacity=cap, out=images, profiler=prof,
@@ -367,7 +393,7 @@ def run_b200(args):
                                    f"{W}x{H}, orbit views (BASELINE.json configs[2])",
                        "gaussians": n, "width": W, "height": H, "views_per_gpu": V,
                        "parallelism": f"view-parallel x{world}", "projection_dtype": "f64",
-                       "composite_dtype": "f32",
+                       "composite_dtype": "f32", "composite_exp": args.exp,
                        "l2": "inputs larger than L2 (352 MB of prepared records re-read per view)"},
             "gaussians_per_s": views_per_s * n,
             "stage_ms_per_view": {k: v / max(nviews, 1) for k, v in stage_ms.items()},
@@ -375,7 +401,11 @@ def run_b200(args):
             "overflowed_views": overflow,
             "prep_ms": prep_ms, "broadcast_ms": bcast_ms,
             "view_algorithmic_gbs": view_bytes * views_per_s / world / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_composite<float,128,2>",
+            "other_exp_mode": {"exp": other.exp_mode,
+                               "value": world * V / (float(t_other.item()) / 1e3),
+                               "framebuffer_vs_headline": mode_diff},
+            "roofline": {"bound": "hbm",
+                         "kernel": "k_composite<float,128,2,%s>" % ("true" if args.exp == "fast" else "false"),
                          "achieved": comp_gbs, "peak": peak, "unit": "GB/s",
                          "frac": comp_gbs / peak, "traffic": traffic,
                          "peak_source": peak_kind,

@@ -89,6 +89,13 @@ typedef struct g6r_config {
     int32_t precision;   /* 0: f32 framebuffer, 1: f64 (raster.py:93) */
     double low_pass;     /* px^2 added to the cov2d diagonal (raster.py:90) */
     double alpha_max;    /* per-splat alpha cap (raster.py:91) */
+    /* Compositor exp in the f32 framebuffer: 0 = glibc expf restated exactly
+     * (framebuffer bit-identical to the reference's, _kernels.pyx:29-33);
+     * 1 = SFU ex2 (image within ~1e-6 relative of mode 0, far inside the
+     * 1e-3 max-abs / 60 dB PSNR parity bound; every alpha-floor decision is
+     * still exact).  Ignored for f64 and for RGBA8 frames (always exact). */
+    int32_t exp_mode;
+    int32_t reserved;    /* 0 */
 } g6r_config;
 
 /* Device-resident scene after g6r_prepare. */

@@ -60,7 +60,8 @@ class Camera(ctypes.Structure):
 
 
 class Config(ctypes.Structure):
-    _fields_ = [("tile_size", I32), ("precision", I32), ("low_pass", D), ("alpha_max", D)]
+    _fields_ = [("tile_size", I32), ("precision", I32), ("low_pass", D), ("alpha_max", D),
+                ("exp_mode", I32), ("reserved", I32)]
 
 
 class Scene(ctypes.Structure):

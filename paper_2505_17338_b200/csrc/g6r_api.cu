@@ -112,6 +112,8 @@ static int check_config(const g6r_config *cfg) {
         return fail(G6R_EINVAL, "tile_size must lie in [1, 32], got %d", cfg->tile_size);
     if (cfg->precision != 0 && cfg->precision != 1)
         return fail(G6R_EINVAL, "precision must be 0 (f32) or 1 (f64), got %d", cfg->precision);
+    if (cfg->exp_mode != 0 && cfg->exp_mode != 1)
+        return fail(G6R_EINVAL, "exp_mode must be 0 (exact) or 1 (fast), got %d", cfg->exp_mode);
     return G6R_OK;
 }
 
@@ -141,6 +143,7 @@ static int make_view(const g6r_camera *cam, const g6r_config *cfg, ViewParams &v
     vp.tiles_x = (cam->width + cfg->tile_size - 1) / cfg->tile_size;
     vp.tiles_y = (cam->height + cfg->tile_size - 1) / cfg->tile_size;
     vp.precision = cfg->precision;
+    vp.exp_mode = cfg->exp_mode;
     return G6R_OK;
 }
 

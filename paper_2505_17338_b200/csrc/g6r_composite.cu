@@ -191,7 +191,7 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // warp's pixel block; warps then ballot over the batch and visit only splats
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
-template <typename Real, int kNB, int kSub = 1>
+template <typename Real, int kNB, int kSub = 1, bool kFastExp = false>
 __global__ void __launch_bounds__(kNB > 0 ? kNB : 1024)
 k_composite(const __grid_constant__ Batch bt, int sorted) {
     using S = typename Px<Real>::S;
@@ -318,7 +318,18 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                     // power_lo >= -4.5: below it the alpha floor rejects the
                     // pixel anyway, so the expf is skipped, no bit changes
                     if (pw > (Real)0 || pw < power_lo(s)) continue;
-                    const Real ai = al * splat_exp_s(pw, eops);
+                    Real ai;
+                    if constexpr (kFastExp && sizeof(Real) == 4) {
+                        // SFU 2^x: <= ~7e-7 relative from the exact path (ex2
+                        // 2 ulp + the rounding of pw * log2 e for |pw| <= 4.5);
+                        // inside 2e-6 of the floor the exact expf decides
+                        float e;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
+                        ai = al * e;
+                        if (fabsf(ai - floor_a) <= 2e-6f * floor_a) ai = al * splat_exp_s(pw, eops);
+                    } else {
+                        ai = al * splat_exp_s(pw, eops);
+                    }
                     if (ai < floor_a) continue;
                     Real r, g, b;
                     colours(s, r, g, b);
@@ -504,7 +515,12 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         else
             k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
-        if (vp.tile_size == 16)
+        bool fast = vp.exp_mode == 1;
+        for (int v = 0; v < b.nviews; ++v) fast = fast && !b.out[v].rgba8;   // served bytes stay exact
+        if (vp.tile_size == 16 && fast)
+            k_composite<float, 256 / kCompositeSub, kCompositeSub, true>
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16)
             k_composite<float, 256 / kCompositeSub, kCompositeSub>
                 <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
         else

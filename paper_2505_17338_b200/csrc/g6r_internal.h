@@ -51,7 +51,7 @@ struct ViewParams {
     double rot[9];
     double focal, cx, cy, znear, zfar, lim_x, lim_y, width, height;
     double low_pass, alpha_max;
-    int32_t iw, ih, tile_size, tiles_x, tiles_y, precision;
+    int32_t iw, ih, tile_size, tiles_x, tiles_y, precision, exp_mode;
 };
 
 struct ViewOut {

@@ -70,6 +70,19 @@ def test_abi_rejects_bad_arguments_before_touching_the_device():
     rc = lib.g6r_render(ctypes.byref(sc0), 0xFFFF, ctypes.byref(cam), ctypes.byref(cfg), None, 0,
                         1024, ctypes.byref(fr1), None, None)
     assert rc == nat.G6R_EINVAL and b"workspace" in lib.g6r_last_error()
+    bad_exp = nat.Config(16, 0, 0.3, 0.99, 2, 0)
+    rc = lib.g6r_render(ctypes.byref(sc0), 0xFFFF, ctypes.byref(cam), ctypes.byref(bad_exp), None, 0,
+                        0, ctypes.byref(fr1), None, None)
+    assert rc == nat.G6R_EINVAL and b"exp_mode" in lib.g6r_last_error()
+
+
+def test_exp_mode_is_validated_on_the_host():
+    from paper_2505_17338_b200 import raster
+    from paper_2505_17338_b200.errors import InvalidParameterError
+    assert raster._check_config(raster.RenderConfig(exp_mode="fast")).exp_mode == 1
+    assert raster._check_config(raster.RenderConfig()).exp_mode == 0
+    with pytest.raises(InvalidParameterError):
+        raster._check_config(raster.RenderConfig(exp_mode="approx"))
 
 
 def test_check_maps_codes_to_exceptions():
