@@ -9,7 +9,8 @@ timeout 300 python bench.py --steps 16 --warmup 3 --no-cpu-baseline > gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 16 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_list_${TAG}.log 2>&1
 for K in k_composite k_project k_onesweep k_sort_hist k_chunk_scatter k_chunk_count; do
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$K" -s 3 -c 1 \
+  S=3; [ "$K" = k_onesweep ] && S=5
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$K" -s $S -c 1 \
       -o gpurun_out/full_${TAG}_${K} python tools/probe_sort.py > gpurun_out/ncu_full_${TAG}_${K}.log 2>&1
 done
 ls -la gpurun_out
