@@ -518,8 +518,8 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
     return _launch(prep, bits, camera, config, False, int(capacity or prep.entry_hint))
 
 
-DEFAULT_CONCURRENCY = 8   # views per batched launch (g6r_render_views)
-MAX_BATCH = 16            # kMaxBatch in csrc/g6r_internal.h
+DEFAULT_CONCURRENCY = 16  # views per batched launch (g6r_render_views)
+MAX_BATCH = 32            # kMaxBatch in csrc/g6r_internal.h
 PIPELINE_LANES = int(os.environ.get("G6R_LANES", "2"))   # streams batches alternate over (<= 4)
 
 
