@@ -8,6 +8,10 @@ bench.py's roofline.traffic."""
 import csv, io, json, subprocess, sys
 
 views, out, reps = int(sys.argv[1]), sys.argv[2], sys.argv[3:]
+try:
+    PEAK_GBPS = float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
+except Exception:
+    PEAK_GBPS = 6548.5
 want = {"gpu__time_duration.sum": "duration_us", "dram__bytes_read.sum": "dram_read_MB",
         "dram__bytes_write.sum": "dram_write_MB", "lts__t_sector_hit_rate.pct": "l2_hit_pct",
         "launch__registers_per_thread": "registers", "launch__grid_size": "grid",
@@ -51,6 +55,11 @@ for rep in reps:
                    float(d[k] or 0)) for k in h
                   if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
         ent["top_stalls"] = dict(sorted(stalls, key=lambda t: -t[1])[:4])
+        if ent.get("duration_us") and ent.get("dram_read_MB") is not None:
+            # achieved DRAM bandwidth of this capture against the measured copy peak
+            gbs = (ent["dram_read_MB"] + ent["dram_write_MB"]) * 1e6 / (ent["duration_us"] * 1e-6) / 1e9
+            ent["dram_GBps"] = gbs
+            ent["dram_frac_of_peak"] = gbs / PEAK_GBPS
         res[name] = ent
 summary = {"views_per_launch": views, "kernels": res}
 comp = next((v for k, v in res.items() if k.startswith("k_composite")), None)
