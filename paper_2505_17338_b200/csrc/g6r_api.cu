@@ -42,7 +42,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_counts, rect, chunk_hist, tile_total, total;
+        sort_counts, rect, chunk_hist, warp_prefix, tile_total, total;
     int64_t sort_tiles_cap;
 };
 
@@ -79,6 +79,9 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + (size_t)n * sizeof(uint2));
     L.chunk_hist = o;
     o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, chunk_splats(tiles)) * tiles * sizeof(unsigned));
+    L.warp_prefix = o;   // kScatterWarps x ceil(T/2) packed words per chunk
+    o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, chunk_splats(tiles)) * kScatterWarps * ((tiles + 1) / 2) *
+                         sizeof(unsigned));
     L.tile_total = o;
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.total = o;
@@ -100,6 +103,7 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.sort_counts = reinterpret_cast<unsigned *>(b + L.sort_counts);
     w.rect = reinterpret_cast<uint2 *>(b + L.rect);
     w.chunk_hist = reinterpret_cast<unsigned *>(b + L.chunk_hist);
+    w.warp_prefix = reinterpret_cast<unsigned *>(b + L.warp_prefix);
     w.tile_total = reinterpret_cast<unsigned *>(b + L.tile_total);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;

@@ -29,6 +29,7 @@ struct Workspace {
     int4 *splat_rect;               // optional (backward): per splat (entry offset, x0, y0, wx)
     uint2 *rect;                    // splat-sort path: per scene row (x0 | y0 << 16, wx | hy << 16)
     unsigned *chunk_hist;           // splat-sort path: per chunk of sorted splats, T tile counts
+    unsigned *warp_prefix;          // splat-sort path: per chunk, per scatter warp, packed u16 tile offsets
     unsigned *tile_total;           // splat-sort path: T entry counts
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
@@ -45,6 +46,7 @@ __host__ __device__ inline int chunk_splats(int64_t tiles) {
     return tiles <= 1024 ? kChunkSplats : 4 * kChunkSplats;
 }
 constexpr int kMaxSplatSortTiles = 4096;   // larger tile grids use the entry sort
+constexpr int kScatterWarps = 8;           // warps (slices) per partition chunk
 
 struct ViewParams {
     double pos[3];

@@ -25,7 +25,6 @@
 
 namespace g6r {
 
-constexpr int kScatterWarps = 8;
 
 struct PartCtx {
     int64_t m;             // drawn splats (the first m sorted items)
@@ -105,27 +104,51 @@ __device__ __forceinline__ unsigned group_entry(const EntryGroup &g, int s, int 
     return (unsigned)(((int)(a >> 16) + qy) * tiles_x + (int)(a & 0xffffu) + qx);
 }
 
+// Per chunk: each warp counts the entries of its slice of the chunk (the
+// slices k_chunk_scatter ranks) per tile into packed 16-bit counters; the
+// counters are prefixed over the warps and written out (the scatter's starting
+// offsets inside the chunk), and the chunk's tile totals go to chunk_hist.
 __global__ void __launch_bounds__(kBlock)
 k_chunk_count(const __grid_constant__ Batch b, unsigned long long vmask) {
-    extern __shared__ unsigned s_hist[];
+    extern __shared__ unsigned s_cw[];   // [warps][tw] packed u16 counters
     const int v = blockIdx.y;
     PartCtx c;
     if (!part_ctx(b, v, c) || blockIdx.x >= c.chunks) return;
     const Workspace &ws = b.ws[v];
-    for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) s_hist[t] = 0u;
+    const int T = c.tiles, tw = (T + 1) >> 1;
+    for (int k = threadIdx.x; k < kScatterWarps * tw; k += blockDim.x) s_cw[k] = 0u;
     __syncthreads();
-    const int64_t s0 = (int64_t)blockIdx.x * c.chunk;
-    const int64_t s1 = s0 + c.chunk < c.m ? s0 + c.chunk : c.m;
-    for (int64_t sp = s0 + threadIdx.x; sp < s1; sp += blockDim.x) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = c.chunk / kScatterWarps;
+    const int64_t c0 = (int64_t)blockIdx.x * c.chunk;
+    const int64_t chunk_end = c0 + c.chunk < c.m ? c0 + c.chunk : c.m;
+    const int64_t w0s = c0 + (int64_t)warp * per;
+    const int64_t w1s = w0s + per < chunk_end ? w0s + per : chunk_end;
+    unsigned *cw = s_cw + warp * tw;
+    for (int64_t sp = w0s + lane; sp < w1s; sp += 32) {
         const unsigned row = (unsigned)(c.items[sp] & vmask);
         int x0, y0, wx, hy;
         unpack_rect(ws.rect[row], x0, y0, wx, hy);
         for (int yy = 0; yy < hy; ++yy)
-            for (int xx = 0; xx < wx; ++xx) atomicAdd(&s_hist[(y0 + yy) * c.tiles_x + x0 + xx], 1u);
+            for (int xx = 0; xx < wx; ++xx) {
+                const int t = (y0 + yy) * c.tiles_x + x0 + xx;
+                atomicAdd(&cw[t >> 1], 1u << ((t & 1) * 16));
+            }
     }
     __syncthreads();
-    unsigned *row_out = ws.chunk_hist + (int64_t)blockIdx.x * c.tiles;
-    for (int t = threadIdx.x; t < c.tiles; t += blockDim.x) row_out[t] = s_hist[t];
+    unsigned *pre = ws.warp_prefix + (int64_t)blockIdx.x * kScatterWarps * tw;
+    unsigned *row_out = ws.chunk_hist + (int64_t)blockIdx.x * T;
+    for (int k = threadIdx.x; k < tw; k += blockDim.x) {
+        unsigned run = 0;   // packed pairs: a chunk puts < 65536 entries in a tile
+#pragma unroll
+        for (int w = 0; w < kScatterWarps; ++w) {
+            const unsigned x = s_cw[w * tw + k];
+            pre[w * tw + k] = run;
+            run += x;
+        }
+        row_out[2 * k] = run & 0xffffu;
+        if (2 * k + 1 < T) row_out[2 * k + 1] = run >> 16;
+    }
 }
 
 // Exclusive prefix of every tile column over the chunks, and the tile totals.
@@ -220,16 +243,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const __grid_constant__ Batc
 }
 
 // k_chunk_scatter: CTA = chunk, warp w owns the w-th eighth of the chunk's
-// sorted splats.  Pass 1: each warp counts its entries per tile (16-bit
-// counters, two per shared word, bumped with 32-bit shared atomics; a chunk
-// puts at most chunk_splats(T) <= 8192 entries in one tile, so halves never
-// carry).  The counters are then prefixed over warps in place (the packed
-// words add lane-wise for the same reason) and tile_start + chunk prefix is
-// kept per tile.  Pass 2: each warp walks its splats again in groups of 32,
-// enumerates the group's entries in order 32 at a time (group_entry) and ranks
-// them with match-any on the tile id against its own running counters; the
-// leader of each tile's peers advances the counter.  No CTA
-// barrier inside either pass, and every position is a function of the sorted
+// sorted splats (the slices k_chunk_count counted).  The warp's counters start
+// at k_chunk_count's per-warp prefix (16-bit counters, two per shared word);
+// tile_start + chunk prefix is kept per tile.  Each warp walks its splats in
+// groups of 32, enumerates the group's entries in order 32 at a time
+// (group_entry) and ranks them with match-any on the tile id against its own
+// running counters; the leader of each tile's peers advances the counter.  No
+// CTA barrier after the setup, and every position is a function of the sorted
 // order alone.
 __global__ void __launch_bounds__(kBlock)
 k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
@@ -241,10 +261,14 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     const int T = c.tiles;
     const int tw = (T + 1) >> 1;   // packed counter words per warp
     unsigned *s_tb = reinterpret_cast<unsigned *>(s_raw);                  // [T] tile start + chunk prefix
-    unsigned *s_cw = s_tb + T;                                              // [warps][tw] packed u16 counters
+    unsigned *s_cw = s_tb + ((T + 3) & ~3);                                 // [warps][tw] packed u16 counters
     const unsigned *chunk_off = ws.chunk_hist + (int64_t)blockIdx.x * T;
     for (int t = threadIdx.x; t < T; t += blockDim.x) s_tb[t] = (unsigned)ws.tile_starts[t] + chunk_off[t];
-    for (int k = threadIdx.x; k < kScatterWarps * tw; k += blockDim.x) s_cw[k] = 0u;
+    {   // this chunk's per-warp starting counters (k_chunk_count)
+        const uint4 *pre = reinterpret_cast<const uint4 *>(ws.warp_prefix + (int64_t)blockIdx.x * kScatterWarps * tw);
+        uint4 *dst = reinterpret_cast<uint4 *>(s_cw);
+        for (int k = threadIdx.x; k < kScatterWarps * tw / 4; k += blockDim.x) dst[k] = pre[k];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -255,27 +279,6 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     const int64_t w1s = w0s + per < chunk_end ? w0s + per : chunk_end;
     unsigned *cw = s_cw + warp * tw;
     unsigned short *cnt16 = reinterpret_cast<unsigned short *>(cw);
-    // pass 1: this warp's entries per tile
-    for (int64_t g0 = w0s; g0 < w1s; g0 += 32) {
-        const EntryGroup g = load_group(c, ws, g0 + lane, w1s, vmask);
-        for (int q0 = 0; q0 < g.total; q0 += 32) {
-            unsigned row;
-            const unsigned t = group_entry(g, q0 + lane, c.tiles_x, row);
-            if (q0 + lane < g.total) atomicAdd(&cw[t >> 1], 1u << ((t & 1u) * 16u));
-        }
-    }
-    __syncthreads();
-    // exclusive prefix of the per-warp counts, per tile (packed pairs)
-    for (int k = threadIdx.x; k < tw; k += blockDim.x) {
-        unsigned run = 0;
-#pragma unroll
-        for (int w = 0; w < kScatterWarps; ++w) {
-            const unsigned x = s_cw[w * tw + k];
-            s_cw[w * tw + k] = run;
-            run += x;
-        }
-    }
-    __syncthreads();
     // pass 2: rank and scatter, 32 entries at a time
     unsigned *vals = ws.vals[0];
     for (int64_t g0 = w0s; g0 < w1s; g0 += 32) {
@@ -299,7 +302,7 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
 }
 
 static size_t scatter_smem_bytes(int tiles) {
-    return (size_t)tiles * sizeof(unsigned) + (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
+    return (size_t)((tiles + 3) & ~3) * sizeof(unsigned) + (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
 }
 
 int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st) {
@@ -307,12 +310,12 @@ int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st)
     const int tiles = b.vp[0].tiles_x * b.vp[0].tiles_y;
     const int64_t chunks = ceil_div(n > 0 ? n : 1, chunk_splats(tiles));
     const unsigned long long vmask = (1ull << vbits) - 1ull;
-    const size_t count_smem = (size_t)tiles * sizeof(unsigned);
+    const size_t count_smem = (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
     const size_t scatter_smem = scatter_smem_bytes(tiles);
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(k_chunk_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kMaxSplatSortTiles * sizeof(unsigned)));
+                             (int)(kScatterWarps * (kMaxSplatSortTiles / 2) * sizeof(unsigned)));
         cudaFuncSetAttribute(k_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)scatter_smem_bytes(kMaxSplatSortTiles));
         attrs = true;
