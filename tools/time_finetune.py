@@ -33,7 +33,7 @@ def main():
     cams = scenes.orbit_ring(scene, count=a.views, size=a.size)
     views = [(c, scenes.synthetic_target(a.size, a.size, seed=k)) for k, c in enumerate(cams)]
     t_build = time.time() - t0
-    tr = D.DeviceTrainer(scene, views, total_steps=300)
+    tr = D.DeviceTrainer(scene, views, total_steps=max(300, a.iters + 3))
     rng = np.random.default_rng(0)
     for _ in range(3):
         tr.step(int(rng.integers(len(views))))
