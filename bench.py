@@ -401,6 +401,9 @@ def run_b200(args):
             "overflowed_views": overflow,
             "prep_ms": prep_ms, "broadcast_ms": bcast_ms,
             "view_algorithmic_gbs": view_bytes * views_per_s / world / 1e9,
+            # whole path (180 N + 64 M + 84 E + 8 T + 16 HW bytes per view)
+            # per GPU against the measured HBM copy peak
+            "view_roofline_frac": view_bytes * views_per_s / world / 1e9 / peak,
             "other_exp_mode": {"exp": other.exp_mode,
                                "value": world * V / (float(t_other.item()) / 1e3),
                                "framebuffer_vs_headline": mode_diff},
