@@ -213,7 +213,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     unsigned *smask = kNB > 0 ? s_mask_static : reinterpret_cast<unsigned *>(sp + 2 * nb);
     __shared__ unsigned long long s_tab[32];
     __shared__ float4 s_wbox[32];   // pixel-centre box per warp
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
+    for (int k = threadIdx.x; k < 32; k += blockDim.x) s_tab[k] = c_expf_tab[k];   // tiles below 6x6 have < 32 threads
     const uint32_t sp_base = smem_addr(sp), mask_base = smem_addr(smask);
     const ExpOperands eops = exp_operands(smem_addr(s_tab));
 
@@ -463,7 +463,7 @@ __global__ void k_composite_backward(ViewParams vp, const double *__restrict__ m
 
 __global__ void k_debug_expf(int64_t n, const float *x, float *y) {
     __shared__ unsigned long long s_tab[32];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = c_expf_tab[threadIdx.x];
+    for (int k = threadIdx.x; k < 32; k += blockDim.x) s_tab[k] = c_expf_tab[k];
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
