@@ -62,3 +62,29 @@ def test_fuzz_against_oracle(oracle, seed):
     fast = raster.render(s, cam, mask, config=RenderConfig(tile_size=tile, exp_mode="fast"))
     want32 = oracle.render_with_state(sub, cam, None, "f32", tile_size=tile).image
     assert_image_close(fast, want32)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_large_images_against_oracle(oracle, seed):
+    """Large and fine tile grids (up to ~140k tiles: the entry-sort fallback of
+    render_views, wide radix keys) with dense scenes."""
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.choice([2500, 12000]))
+    box = float(rng.uniform(10.0, 25.0))
+    s = scenes.random_scene(rng, n, box=box)
+    w, h = int(rng.integers(400, 1500)), int(rng.integers(400, 1500))
+    tile = int(rng.choice([4, 8, 16, 32] if n < 10000 else [16, 32]))   # E stays < ~30M
+    cam = scenes.orbit_camera(azimuth=float(rng.uniform(0, 2 * math.pi)),
+                              elevation=float(rng.uniform(-1.0, 1.0)),
+                              distance=float(rng.uniform(2.5, 4.0)) * box, width=w, height=h)
+    cfg = RenderConfig(tile_size=tile)
+    want = oracle.render_with_state(s, cam, None, "f32", tile_size=tile)
+    st = raster.render_with_state(s, cam, config=cfg)
+    np.testing.assert_array_equal(st.entries.tile_starts, want.entries.tile_starts)
+    np.testing.assert_array_equal(st.entries.entry_splat, want.entries.entry_splat)
+    np.testing.assert_array_equal(st.image, want.image)
+    imgs, cnt = raster.render_views(s, [cam] * 3, config=cfg)
+    for k in range(3):
+        np.testing.assert_array_equal(imgs[k].cpu().numpy(), want.image)
+    fast, _ = raster.render_views(s, [cam], config=RenderConfig(tile_size=tile, exp_mode="fast"))
+    assert_image_close(fast[0].cpu().numpy(), want.image)
