@@ -357,6 +357,26 @@ def run_b200(args):
     for k in range(e2e_views):
         raster.render(scene, cams[k], config=cfg)
     single_s = time.perf_counter() - t0
+    # N > 1: served uint8 frames of every rank's block gathered on rank 0 in
+    # view order (optional), timed apart from the render
+    frame_gather = None
+    if world > 1:
+        try:
+            frames = raster.render_frames_u8(scene, cams, config=cfg, batch=args.concurrency,
+                                             device_out=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            multigpu.gather_frames(frames, world * len(cams), dst=0)
+            torch.cuda.synchronize()
+            tg = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+            gb = world * len(cams) * frames[0].numel()
+            frame_gather = {"views": world * len(cams), "bytes": gb, "ms": float(tg.item()) * 1e3,
+                            "GBps": gb / float(tg.item()) / 1e9}
+            del frames
+        except Exception as exc:   # reported, never fatal to the render measurement
+            frame_gather = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     te = torch.tensor([e2e_s, single_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -424,6 +444,7 @@ def run_b200(args):
                            "pinned D2H overlapped with rendering)",
                     "single_view_render_per_s": world * e2e_views / single_s},
             "gpu_launches": launches,
+            **({"frame_gather": frame_gather} if frame_gather is not None else {}),
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline and host_scene is not None:

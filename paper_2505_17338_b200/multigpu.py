@@ -103,3 +103,28 @@ def broadcast_scene(scene, device, src: int = 0, group=None) -> DeviceScene:
     dist.broadcast(labels, src, group=group)
     dist.broadcast(scales, src, group=group)
     return unpack_scene(params, labels, scales)
+
+
+def gather_frames(frames: torch.Tensor, n_views: int, dst: int = 0, group=None):
+    """Collect every rank's block of served frames on ``dst`` (SURVEY.md 8e,
+    "optionally gather uint8 frames to rank 0").
+
+    ``frames`` holds this rank's ``shard_views`` block, (V_r, H, W, 4) on its
+    device (the blocks differ in length by at most one).  Each rank sends one
+    block padded to ceil(n_views / world) views through a single gather; rank
+    ``dst`` returns the (n_views, H, W, 4) frames in view order, the others
+    None.  Not part of the view-parallel render itself (no data-path
+    collective); the bench times it separately."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = shard_views(n_views, world, rank)
+    if frames.shape[0] != len(mine):
+        raise ValueError(f"rank {rank} holds {frames.shape[0]} frames, its block has {len(mine)}")
+    per = -(-n_views // world)
+    buf = torch.zeros((per,) + tuple(frames.shape[1:]), dtype=frames.dtype, device=frames.device)
+    buf[:len(mine)] = frames
+    out = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+    dist.gather(buf, out, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([out[r][:len(shard_views(n_views, world, r))] for r in range(world)])

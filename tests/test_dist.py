@@ -54,6 +54,34 @@ def test_broadcast_and_shard_world2(tmp_path):
         assert (tmp_path / f"rank{r}").read_text() == "ok"
 
 
+def _gather_worker(rank, world, port, result_dir):
+    """Served-frame gather: rank r's block of views reaches rank 0 in view order."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 7   # blocks of 3 and 4 views
+        mine = multigpu.shard_views(n, world, rank)
+        frames = torch.stack([torch.full((5, 6, 4), v, dtype=torch.uint8) for v in mine])
+        got = multigpu.gather_frames(frames, n, dst=0)
+        if rank == 0:
+            ok = got is not None and got.shape == (n, 5, 6, 4) and all(
+                bool((got[v] == v).all()) for v in range(n))
+        else:
+            ok = got is None
+        with open(os.path.join(result_dir, f"g{rank}"), "w") as fh:
+            fh.write("ok" if ok else "bad")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_frames_world2(tmp_path):
+    world = 2
+    mp.spawn(_gather_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert (tmp_path / f"g{r}").read_text() == "ok"
+
+
 def _dp_worker(rank, world, port, result_dir):
     """Data-parallel fine-tune host logic: the view schedule is identical on
     every rank and the bucketed gradient all-reduce averages in place."""
