@@ -37,6 +37,11 @@ CASES = [
      dict(tile_size=8)),
     ("cull100", 13, 100, dict(azimuth=0.0, elevation=0.0, width=64, height=64), {}),
     ("ties50", 14, 50, dict(azimuth=2.1, elevation=0.3, width=64, height=64), {}),
+    # wider sweeps (round 3): bigger scenes, steep and low poses, non-square frames
+    ("rand1500_wide", 21, 1500, dict(azimuth=3.5, elevation=0.9, width=160, height=96), {}),
+    ("rand2000_low", 22, 2000, dict(azimuth=-2.4, elevation=-1.0, width=112, height=128), {}),
+    ("rand800_raw", 23, 800, dict(azimuth=0.3, elevation=0.5, width=100, height=140),
+     dict(w_mode="raw")),
 ]
 
 
@@ -95,7 +100,8 @@ def make_case(name, seed, n, cam_kw, cfg_kw):
     print(name, "M", st.stats.n_drawn, "E", st.stats.n_entries)
 
 
-BACKWARD_CASES = ("rand40", "rand400", "rand400_raw", "cull100")
+BACKWARD_CASES = ("rand40", "rand400", "rand400_raw", "cull100", "rand1500_wide", "rand2000_low",
+                  "rand800_raw")
 
 
 def make_backward(name):
@@ -199,6 +205,13 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "train":
         make_loss()
         make_finetune()
+        sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[1] == "cases":   # only the named cases (+ their backward)
+        for case in CASES:
+            if case[0] in sys.argv[2:]:
+                make_case(*case)
+                if case[0] in BACKWARD_CASES:
+                    make_backward(case[0])
         sys.exit(0)
     only_bwd = len(sys.argv) > 1 and sys.argv[1] == "backward"
     if not only_bwd:
