@@ -6,8 +6,8 @@
 //                                              -> k_splat_grad_sum
 //   _backward_rows (diffrender.py:183-398)     -> k_backward_rows
 // Deterministic by construction (no floating-point atomics): every entry's
-// gradient row is reduced over the tile's pixels in a fixed order (xor-shuffle
-// tree inside a warp, warps in index order) and written once, to the entry's
+// gradient row is reduced over the tile's pixels in a fixed order (a transposed
+// sum through shared memory inside a warp, warps in index order) and written once, to the entry's
 // pre-sort slot; a splat's rows are then summed sequentially in ascending tile
 // order -- the order np.add.at visits them in the reference.  Results match
 // the reference to rounding (different association of the pixel sums), not
@@ -25,12 +25,6 @@ struct BwdSplat {
     double mx, my, ca, cb, cc, alpha, r, g, b;
 };
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 // One CTA per tile (16x16 -> 8x4 warp blocks, as the forward), one thread per
 // pixel; the run is swept back to front from the tile's largest last_contrib.
 __global__ void __launch_bounds__(256)
@@ -43,6 +37,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
     __shared__ int s_orig[kBwdBatch];
     __shared__ unsigned s_mask[kBwdBatch];
     __shared__ double s_part[8][kBwdBatch][9];
+    __shared__ double s_red[8][9][33];   // per-warp transpose of the 9 partials
     __shared__ unsigned char s_hit[8][kBwdBatch];
     __shared__ float4 s_wbox[8];
     __shared__ int s_maxlast;
@@ -146,11 +141,26 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                 if (lane == 0) s_hit[warp][j] = 0;
                 continue;
             }
+            // transpose through shared memory: lane 3k+p sums 11 (p < 2) or 10
+            // lanes' values of component k in lane order, then p = 0 adds the
+            // other two parts -- a fixed order (deterministic), ~40 issue slots
+            // instead of 9 xor-shuffle trees of f64 (~135)
+            double *red = &s_red[warp][0][0];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                const double v = warp_sum(c[k]);
-                if (lane == 0) s_part[warp][j][k] = v;
+            for (int k = 0; k < 9; ++k) red[k * 33 + lane] = c[k];
+            __syncwarp();
+            double part = 0.0;
+            const int rk = lane / 3, rp = lane - 3 * (lane / 3);
+            if (lane < 27) {
+                const double *row = red + rk * 33 + rp * 11;
+                const int len = rp < 2 ? 11 : 10;
+                part = row[0];
+                for (int q = 1; q < len; ++q) part += row[q];
             }
+            const double p1 = __shfl_down_sync(0xffffffffu, part, 1);
+            const double p2 = __shfl_down_sync(0xffffffffu, part, 2);
+            if (lane < 27 && rp == 0) s_part[warp][j][rk] = (part + p1) + p2;
+            __syncwarp();
         }
         __syncthreads();
         for (int q = threadIdx.x; q < cnt * 9; q += blockDim.x) {   // warps in index order
