@@ -53,26 +53,30 @@ __global__ void k_products(const double *__restrict__ x, const double *__restric
 
 // 1-D correlation with the window along one axis of `planes` (h, w) planes.
 // valid: out length n - 10; full: n + 10 (zero padding, the adjoint).
+// grid (column blocks, output rows, planes): no index division; the taps are
+// summed in the same order as before (k ascending), so the result is unchanged
 __global__ void k_corr1d(const double *__restrict__ in, double *__restrict__ out, int planes, int h,
                          int w, int axis, int full) {
     const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
     const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
-    const int64_t per = (int64_t)oh * ow;
     const int shift = full ? kWin - 1 : 0;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < per * planes;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int p = (int)(q / per);
-        const int64_t r = q % per;
-        const int i = (int)(r / ow), j = (int)(r % ow);
-        const double *src = in + (int64_t)p * h * w;
-        double s = 0.0;
-        for (int k = 0; k < kWin; ++k) {
-            const int ii = axis == 0 ? i + k - shift : i;
-            const int jj = axis == 1 ? j + k - shift : j;
-            if (ii >= 0 && ii < h && jj >= 0 && jj < w) s += c_win[k] * src[(int64_t)ii * w + jj];
-        }
-        out[q] = s;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, p = blockIdx.z;
+    if (j >= ow || i >= oh || p >= planes) return;
+    const double *src = in + (int64_t)p * h * w;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) {
+        const int ii = axis == 0 ? i + k - shift : i;
+        const int jj = axis == 1 ? j + k - shift : j;
+        if (ii >= 0 && ii < h && jj >= 0 && jj < w) s += c_win[k] * src[(int64_t)ii * w + jj];
     }
+    out[((int64_t)p * oh + i) * ow + j] = s;
+}
+
+static dim3 corr_grid(int planes, int h, int w, int axis, int full) {
+    const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
+    const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
+    return dim3((unsigned)((ow + 127) / 128), (unsigned)std::max(oh, 1), (unsigned)planes);
 }
 
 // SSIM window maps (_ssim.py:66-84) from the 5 correlated statistics
@@ -364,8 +368,8 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
                 double *stats = reinterpret_cast<double *>(base + L.stats);
                 double *tmp = reinterpret_cast<double *>(base + L.tmp);
                 k_products<<<grid_for(hwj), 256, 0, st>>>(xs[j], ys[j], hwj, stats);
-                k_corr1d<<<grid_for(5 * (int64_t)hv * wj), 256, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0);
-                k_corr1d<<<grid_for(5 * nv), 256, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0);
+                k_corr1d<<<corr_grid(5, hj, wj, 0, 0), 128, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0);
+                k_corr1d<<<corr_grid(5, hv, wj, 1, 0), 128, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0);
                 k_ssim_maps<<<grid_for(nv), 256, 0, st>>>(stats, nv, mp[j]);
                 if (j == ns - 1) dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, part, chan + j, st);
                 else dsum(mp[j] + 5 * nv, nullptr, nv, part, chan + j, st);
@@ -392,8 +396,8 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
                 double *tmp = reinterpret_cast<double *>(base + L.tmp);
                 double *adj = reinterpret_cast<double *>(base + L.adj);
                 k_ssim_bwd_maps<<<grid_for(nv), 256, 0, st>>>(mp[j], nv, chan + 6 + j, j == ns - 1, gm);
-                k_corr1d<<<grid_for(3 * (int64_t)hj * wv), 256, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
-                k_corr1d<<<grid_for(3 * hwj), 256, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
+                k_corr1d<<<corr_grid(3, hv, wv, 0, 1), 128, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
+                k_corr1d<<<corr_grid(3, hj, wv, 1, 1), 128, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
                 k_ssim_bwd_combine<<<grid_for(hwj), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g);
             }
             // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
