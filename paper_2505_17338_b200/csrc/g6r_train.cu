@@ -8,6 +8,8 @@
 // block partials, then one ordered final sum); Adam follows the reference's
 // operation order element for element.
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <vector>
 
@@ -214,7 +216,7 @@ static unsigned grid_for(int64_t n) {
 // --- host orchestration -------------------------------------------------------
 
 struct LossLayout {
-    size_t x[5], y[5], maps[5], stats, tmp, gm, adj, g, part, scal, absd, total;
+    size_t x[5], y[5], maps[5], stats, tmp, gm, adj, g, part, scal, absd, in_pred, in_tgt, out_grad, total;
 };
 
 static inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
@@ -252,6 +254,14 @@ static LossLayout loss_layout(int h, int w, int scales) {
     o = al(o + 64 * 8);
     L.absd = o;
     o = al(o + 3 * hw * 8);
+    // fixed-address copies of the call's pred / target / gradient, so the
+    // captured graph of the loss can be replayed for any caller buffers
+    L.in_pred = o;
+    o = al(o + 4 * hw * 8);
+    L.in_tgt = o;
+    o = al(o + 4 * hw * 8);
+    L.out_grad = o;
+    o = al(o + 4 * hw * 8);
     L.total = o;
     return L;
 }
@@ -312,19 +322,11 @@ __global__ void k_loss_parts(double *scal, int use_ssim, double lambda_l1, doubl
     scal[kSlotParts + 2] = ssim_loss;
 }
 
-int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
-              double lambda_ssim, int scales, const double *weights_in, void *ws, double *grad,
-              double *parts, cudaStream_t st) {
-    static bool win_set[64] = {};   // __constant__ lives per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return G6R_EINVAL;
-    if (!win_set[dev]) {
-        double wv[kWin];
-        window_host(wv);
-        cudaMemcpyToSymbol(c_win, wv, sizeof wv);
-        win_set[dev] = true;
-    }
+// Every kernel of one loss evaluation, asynchronous on st (graph-capturable);
+// the scalar parts end in scal[kSlotParts..] on the device.
+static void loss_launch(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
+                        double lambda_ssim, int scales, const double *weights_in, void *ws,
+                        double *grad, cudaStream_t st) {
     char *base = static_cast<char *>(ws);
     const int64_t hw = (int64_t)h * w;
     const LossLayout L = loss_layout(h, w, 5);
@@ -405,6 +407,90 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
         }
     }
     k_loss_parts<<<1, 32, 0, st>>>(scal, lambda_ssim > 0.0, lambda_l1, lambda_ssim, (double)(hw * 3));
+}
+
+// The ~150 small kernels of one loss evaluation are captured once per
+// (device, workspace, image size, channels, weights) into a CUDA graph on a
+// private stream and replayed: one launch instead of ~150, same kernels in the
+// same order, hence the same bits.  The caller's buffers are copied to / from
+// fixed workspace regions around the replay.
+struct LossGraph {
+    int dev, h, w, tc, scales;
+    double l1, ssim, weights[5];
+    void *ws;
+    cudaStream_t stream;
+    cudaEvent_t in, out;
+    cudaGraphExec_t exec;
+};
+static std::vector<LossGraph> g_loss_graphs;
+static std::mutex g_loss_mu;
+
+int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
+              double lambda_ssim, int scales, const double *weights_in, void *ws, double *grad,
+              double *parts, cudaStream_t st) {
+    static bool win_set[64] = {};   // __constant__ lives per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return G6R_EINVAL;
+    if (!win_set[dev]) {
+        double wv[kWin];
+        window_host(wv);
+        cudaMemcpyToSymbol(c_win, wv, sizeof wv);
+        win_set[dev] = true;
+    }
+    char *base = static_cast<char *>(ws);
+    const int64_t hw = (int64_t)h * w;
+    const LossLayout L = loss_layout(h, w, 5);
+    double *scal = reinterpret_cast<double *>(base + L.scal);
+    double *ipred = reinterpret_cast<double *>(base + L.in_pred);
+    double *itgt = reinterpret_cast<double *>(base + L.in_tgt);
+    double *ograd = reinterpret_cast<double *>(base + L.out_grad);
+    std::lock_guard<std::mutex> lock(g_loss_mu);   // one replay of a graph at a time
+    LossGraph *gr = nullptr;
+    for (auto &g : g_loss_graphs) {
+        bool same = g.dev == dev && g.h == h && g.w == w && g.tc == tc && g.scales == scales &&
+                    g.l1 == lambda_l1 && g.ssim == lambda_ssim && g.ws == ws;
+        for (int j = 0; same && j < scales; ++j) same = g.weights[j] == weights_in[j];
+        if (same) {
+            gr = &g;
+            break;
+        }
+    }
+    if (!gr) {
+        LossGraph g{};
+        g.dev = dev;
+        g.h = h;
+        g.w = w;
+        g.tc = tc;
+        g.scales = scales;
+        g.l1 = lambda_l1;
+        g.ssim = lambda_ssim;
+        for (int j = 0; j < scales; ++j) g.weights[j] = weights_in[j];
+        g.ws = ws;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&g.in, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&g.out, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            loss_launch(ipred, itgt, tc, h, w, lambda_l1, lambda_ssim, scales, weights_in, ws, ograd,
+                        g.stream);
+            ok = cudaStreamEndCapture(g.stream, &graph) == cudaSuccess &&
+                 cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) return G6R_ECUDA;
+        g_loss_graphs.push_back(g);
+        gr = &g_loss_graphs.back();
+    }
+    cudaMemcpyAsync(ipred, pred, (size_t)hw * 4 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(itgt, tgt, (size_t)hw * tc * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaEventRecord(gr->in, st);
+    cudaStreamWaitEvent(gr->stream, gr->in, 0);
+    cudaGraphLaunch(gr->exec, gr->stream);
+    cudaEventRecord(gr->out, gr->stream);
+    cudaStreamWaitEvent(st, gr->out, 0);
+    cudaMemcpyAsync(grad, ograd, (size_t)hw * 4 * sizeof(double), cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(parts, scal + kSlotParts, 3 * sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);   // the one read-back of the call
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
