@@ -298,7 +298,10 @@ int g6r_filter_rows(int64_t n, const uint8_t *labels, uint32_t group_mask, const
  * weights (host, `scales` entries) are normalised here over the effective
  * scale count; images under 2^(scales-1)*11 px per side use single-scale
  * SSIM.  parts (host, 3) = {total, l1, ssim_loss}.  Synchronises the stream
- * (the scalar reductions are read back).  Deterministic. */
+ * (the scalar reductions are read back).  Deterministic.  The kernel sequence
+ * is captured into a CUDA graph on first use for a given (workspace, size,
+ * weights) and replayed afterwards; pred/target/grad_out are staged through
+ * the workspace, so any caller buffers work. */
 size_t g6r_loss_workspace_bytes(int32_t width, int32_t height);
 int g6r_loss_grad(const double *pred, const double *target, int32_t target_channels,
                   int32_t width, int32_t height, double lambda_l1, double lambda_ssim,
