@@ -487,8 +487,8 @@ static BwdLayout bwd_layout(int64_t n, int32_t width, int32_t height, int32_t ti
     o = align_up(o + nn * 8);
     B.rect = o;
     o = align_up(o + nn * 16);
-    B.egrad = o;
-    o = align_up(o + (size_t)(cap > 0 ? cap : 1) * 72);
+    B.egrad = o;   // one 9-double row per entry and per tile band (2)
+    o = align_up(o + (size_t)(cap > 0 ? cap : 1) * 72 * 2);
     B.gsplat = o;
     o = align_up(o + nn * 72);
     B.final_t = o;

@@ -25,32 +25,34 @@ struct BwdSplat {
     double mx, my, ca, cb, cc, alpha, r, g, b;
 };
 
-// One CTA per tile (16x16 -> 8x4 warp blocks, as the forward), one thread per
-// pixel; the run is swept back to front from the tile's largest last_contrib.
-__global__ void __launch_bounds__(256)
+// Two CTAs per tile, one per 16x8 band (8x4 warp blocks, as the forward), one
+// thread per pixel; each band sweeps the run back to front from its own largest
+// last_contrib and writes its own row per entry (egrad + band * cap * 9).
+__global__ void __launch_bounds__(128)
 k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                 const unsigned *vals0, const unsigned *vals1, const long long *internal,
                 const int64_t *__restrict__ starts, const double *__restrict__ final_t,
                 const int32_t *__restrict__ last_contrib, const double *__restrict__ grad_image,
-                const int4 *__restrict__ rect, double *__restrict__ egrad) {
+                const int4 *__restrict__ rect, double *__restrict__ egrad_all, int64_t cap) {
     __shared__ BwdSplat s_sp[kBwdBatch];
     __shared__ int s_orig[kBwdBatch];
     __shared__ unsigned s_mask[kBwdBatch];
-    __shared__ double s_part[8][kBwdBatch][9];
-    __shared__ double s_red[8][9][33];   // per-warp transpose of the 9 partials
-    __shared__ unsigned char s_hit[8][kBwdBatch];
-    __shared__ float4 s_wbox[8];
+    __shared__ double s_part[4][kBwdBatch][9];
+    __shared__ double s_red[4][9][33];   // per-warp transpose of the 9 partials
+    __shared__ unsigned char s_hit[4][kBwdBatch];
+    __shared__ float4 s_wbox[4];
     __shared__ int s_maxlast;
     const int ts = 16;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x >> 1, band = (int)(blockIdx.x & 1) * 8;
+    double *__restrict__ egrad = egrad_all + (int64_t)(blockIdx.x & 1) * cap * 9;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * ts + (warp & 1) * 8 + (lane & 7);
-    const int py = ty * ts + (warp >> 1) * 4 + (lane >> 3);
+    const int py = ty * ts + band + (warp >> 1) * 4 + (lane >> 3);
     const bool inside = px < vp.iw && py < vp.ih;
-    if (threadIdx.x < 8) {
+    if (threadIdx.x < 4) {
         const int w = threadIdx.x;
-        const int x0 = tx * ts + (w & 1) * 8, y0 = ty * ts + (w >> 1) * 4;
+        const int x0 = tx * ts + (w & 1) * 8, y0 = ty * ts + band + (w >> 1) * 4;
         const int x1 = min(x0 + 7, vp.iw - 1), y1 = min(y0 + 3, vp.ih - 1);
         s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
                                            : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
@@ -90,7 +92,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             const float ex = (float)pl.e.y, ey = (float)pl.f.x;
             const float mx = (float)pl.a.x, my = (float)pl.a.y;
             unsigned mk = 0;
-            for (int w = 0; w < 8; ++w) {
+            for (int w = 0; w < 4; ++w) {
                 const float4 bx = s_wbox[w];
                 if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) mk |= 1u << w;
             }
@@ -166,7 +168,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
         for (int q = threadIdx.x; q < cnt * 9; q += blockDim.x) {   // warps in index order
             const int j = q / 9, k = q % 9;
             double v = 0.0;
-            for (int w = 0; w < 8; ++w)
+            for (int w = 0; w < 4; ++w)
                 if (s_hit[w][j]) v += s_part[w][j][k];
             egrad[(int64_t)s_orig[j] * 9 + k] = v;
         }
@@ -177,7 +179,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
 // g_splat[m] = sum of its entries' rows, ascending tile order (np.add.at order).
 __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
                                  const int64_t *counters, const double *__restrict__ egrad,
-                                 double *__restrict__ gsplat) {
+                                 int64_t cap, double *__restrict__ gsplat) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t mm = counters[G6R_CNT_DRAWN];
     if (m >= mm || m >= m_total) return;
@@ -186,9 +188,9 @@ __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
     double acc[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-    for (int64_t i = a; i < b; ++i)
+    for (int64_t i = a; i < b; ++i)   // entry row = upper band + lower band
 #pragma unroll
-        for (int k = 0; k < 9; ++k) acc[k] += egrad[i * 9 + k];
+        for (int k = 0; k < 9; ++k) acc[k] += egrad[i * 9 + k] + egrad[(cap + i) * 9 + k];
 #pragma unroll
     for (int k = 0; k < 9; ++k) gsplat[m * 9 + k] = acc[k];
 }
@@ -443,19 +445,19 @@ int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspac
                     double *g_cov_raw, double *g_sh, double *g_opacity_raw, cudaStream_t st) {
     if (vp.tile_size != 16) return G6R_EINVAL;
     const int64_t n = scene.n;
-    cudaMemsetAsync(egrad, 0, (size_t)ws.entry_capacity * 9 * sizeof(double), st);
+    cudaMemsetAsync(egrad, 0, (size_t)ws.entry_capacity * 9 * 2 * sizeof(double), st);
     cudaMemsetAsync(g_mu_p, 0, (size_t)n * 3 * sizeof(double), st);
     cudaMemsetAsync(g_mu_d, 0, (size_t)n * 3 * sizeof(double), st);
     cudaMemsetAsync(g_cov_raw, 0, (size_t)n * 21 * sizeof(double), st);
     cudaMemsetAsync(g_sh, 0, (size_t)n * 12 * sizeof(double), st);
     cudaMemsetAsync(g_opacity_raw, 0, (size_t)n * sizeof(double), st);
     if (n == 0) return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
-    k_composite_bwd<<<vp.tiles_x * vp.tiles_y, 256, 0, st>>>(
+    k_composite_bwd<<<vp.tiles_x * vp.tiles_y * 2, 128, 0, st>>>(
         vp, static_cast<const PayloadF64 *>(ws.payload), ws.vals[0], ws.vals[1], ws.internal,
-        ws.tile_starts, final_t, last, grad_image, ws.splat_rect, egrad);
+        ws.tile_starts, final_t, last, grad_image, ws.splat_rect, egrad, ws.entry_capacity);
     trace_mark("composite_bwd", st);
     const unsigned grid = (unsigned)ceil_div(n, 128);
-    k_splat_grad_sum<<<grid, 128, 0, st>>>(n, ws.splat_rect, counters, egrad, gsplat);
+    k_splat_grad_sum<<<grid, 128, 0, st>>>(n, ws.splat_rect, counters, egrad, ws.entry_capacity, gsplat);
     trace_mark("splat_grad_sum", st);
     BwdScene sc{mu_p, mu_d, cov_raw, sh, {ss[0], ss[1], ss[2]}, ds, w_mode};
     BwdOut out{g_mu_p, g_mu_d, g_cov_raw, g_sh, g_opacity_raw};
