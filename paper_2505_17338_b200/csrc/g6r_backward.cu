@@ -19,7 +19,10 @@
 
 namespace g6r {
 
-constexpr int kBwdBatch = 32;   // entries staged per backward batch
+#ifndef G6R_BWD_BATCH
+#define G6R_BWD_BATCH 64
+#endif
+constexpr int kBwdBatch = G6R_BWD_BATCH;   // entries staged per backward batch
 
 struct BwdSplat {
     double mx, my, ca, cb, cc, alpha, r, g, b;
