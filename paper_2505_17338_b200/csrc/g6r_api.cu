@@ -360,7 +360,12 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
     if (count == 0) return G6R_OK;
     if (int rc = check_config(cfg)) return rc;
     if (!scene) return fail(G6R_EINVAL, "scene is NULL");
-    const int nb = batch < 1 ? 1 : (batch > kMaxBatch ? kMaxBatch : batch);
+    const int nb_max = batch < 1 ? 1 : (batch > kMaxBatch ? kMaxBatch : batch);
+    // balanced batches: count views in ceil(count / nb_max) launches of (almost)
+    // equal size -- 20 views at 16 run as 10 + 10, not 16 + a 4-view tail whose
+    // heaviest tiles bound a launch of its own
+    const int nbatches = (int)((count + nb_max - 1) / nb_max);
+    const int nb = (int)((count + nbatches - 1) / nbatches);
     const cudaStream_t st = (cudaStream_t)stream;
     // Pipelined when the workspace holds two batches, there are at least two
     // batches, and no profiler is attached (stage timings need one lane).
@@ -701,8 +706,11 @@ int g6r_loss_grad(const double *pred, const double *target, int32_t target_chann
         return fail(G6R_EINVAL, "loss: target must have 3 or 4 channels");
     if (width < 11 || height < 11) return fail(G6R_EINVAL, "loss: images must be >= 11 px per side");
     if (scales < 1 || scales > 5 || !weights) return fail(G6R_EINVAL, "loss: scales must be 1..5");
-    if (lambda_l1 < 0.0 || lambda_ssim < 0.0 || (lambda_l1 == 0.0 && lambda_ssim == 0.0))
-        return fail(G6R_EINVAL, "loss: weights must be non-negative, one positive");
+    if (!std::isfinite(lambda_l1) || !std::isfinite(lambda_ssim) || lambda_l1 < 0.0 ||
+        lambda_ssim < 0.0 || (lambda_l1 == 0.0 && lambda_ssim == 0.0))
+        return fail(G6R_EINVAL, "loss: weights must be finite and non-negative, one positive");
+    for (int j = 0; j < scales; ++j)
+        if (!std::isfinite(weights[j])) return fail(G6R_EINVAL, "loss: scale weights must be finite");
     if (workspace_bytes < loss_workspace_bytes(height, width))
         return fail(G6R_EINVAL, "loss: workspace too small");
     if (loss_grad(pred, target, target_channels, height, width, lambda_l1, lambda_ssim, scales,

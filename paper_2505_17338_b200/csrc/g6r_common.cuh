@@ -165,6 +165,14 @@ __device__ __forceinline__ void cull_extents_f32(float a, float b, float c, floa
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Bit of the current device in a 64-bit per-device "done" mask (function
+// attributes such as the dynamic shared-memory limit are per device/context).
+inline unsigned long long device_bit() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 1ull << (dev & 63);
+}
+
 // --- glibc-compatible expf --------------------------------------------------
 // glibc 2.39 computes expf in double precision: k = round(x * 32/ln2),
 // r = x*32/ln2 - k, 2^(k/32) from a 32-entry table, and a cubic in r

@@ -12,6 +12,7 @@
 // framebuffer matches the reference's bit for bit.  Nothing here is a dense
 // contraction, so it runs on the FP32/FP64 pipes, not tensor cores.
 #include <algorithm>
+#include <atomic>
 
 #include "g6r_common.cuh"
 #include "g6r_internal.h"
@@ -500,13 +501,14 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     const dim3 grid((unsigned)(vp.tiles_x * vp.tiles_y), (unsigned)b.nviews);
     if (grid.x == 0) return G6R_OK;
     const int srt = sorted ? 1 : 0;
-    static bool attrs_set = false;   // > 48 KB dynamic smem for large f64 tiles
-    if (!attrs_set) {
+    // > 48 KB dynamic smem for large f64 tiles; the attribute is per device
+    static std::atomic<unsigned long long> attrs_done{0};
+    if (const unsigned long long bit = device_bit(); !(attrs_done.load() & bit)) {
         cudaFuncSetAttribute(k_composite<double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              2 * 1024 * (int)(sizeof(Px<double>::S) + 4));
         cudaFuncSetAttribute(k_composite<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              2 * 1024 * (int)(sizeof(Px<float>::S) + 4));
-        attrs_set = true;
+        attrs_done.fetch_or(bit);
     }
     if (vp.precision) {
         if (vp.tile_size == 16)

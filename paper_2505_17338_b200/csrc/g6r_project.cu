@@ -508,6 +508,9 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
                               : make_uint2(0u, 0u);
         }
         __syncthreads();
+        // this block's drawn count, for the optional export of the runs as
+        // compacted splat indices (k_rank_scan / k_rank_fill, g6r_tiles.cu)
+        if (threadIdx.x == 0 && s_tot[0]) ws.proj_status[tile] = s_tot[0];
         if (threadIdx.x == 0 && s_tot[0]) {
             atomicAdd((unsigned long long *)&counters[G6R_CNT_DRAWN], (unsigned long long)s_tot[0]);
             atomicAdd((unsigned long long *)&counters[G6R_CNT_ENTRIES], (unsigned long long)s_tot[1]);

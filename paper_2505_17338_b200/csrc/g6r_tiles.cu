@@ -19,6 +19,7 @@
 // Every step is deterministic and keeps the sorted order, so runs, tile starts
 // and images are bit-identical to the entry sort's.
 #include <algorithm>
+#include <atomic>
 
 #include "g6r_common.cuh"
 #include "g6r_internal.h"
@@ -301,6 +302,82 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
     }
 }
 
+// --- optional export of the sorted runs (g6r_frame.entry_splat) --------------
+// The scatter stores scene rows; the reference's entry_splat holds indices
+// into the compacted SplatBatch (drawn rows in ascending scene order,
+// raster.py:279-288, 366-376).  cidx[row] = number of drawn rows before row:
+// the projection left each 256-row block's drawn count in proj_status[block]
+// (k_project, splat-keys mode); k_rank_scan turns the block counts into
+// exclusive offsets, k_rank_fill ranks rows inside a block (drawn <=> the rect
+// is non-empty), k_export_runs maps every entry.  cidx lives in the sort
+// ping-pong buffer that does not hold the sorted items (>= 8n bytes, unused
+// after the partition).  Only views whose frame asks for entry_splat run.
+__device__ __forceinline__ unsigned *rank_buffer(const Workspace &ws) {
+    return reinterpret_cast<unsigned *>(ws.keys[(ws.internal[kSortPasses] & 1) ^ 1]);
+}
+
+__global__ void __launch_bounds__(1024) k_rank_scan(const __grid_constant__ Batch b, int64_t nblk) {
+    __shared__ unsigned long long s_warp[32];
+    __shared__ unsigned long long s_carry;
+    const int v = blockIdx.y;
+    PartCtx c;
+    if (!b.out[v].entry_splat || !part_ctx(b, v, c)) return;
+    unsigned long long *cnt = b.ws[v].proj_status;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t k0 = 0; k0 < nblk; k0 += blockDim.x) {
+        const int64_t k = k0 + threadIdx.x;
+        const unsigned long long x = k < nblk ? cnt[k] : 0ull;
+        const unsigned long long inc = warp_inclusive_scan(x);
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long w = s_warp[lane];
+            s_warp[lane] = warp_inclusive_scan(w) - w;
+        }
+        __syncthreads();
+        const unsigned long long excl = s_carry + s_warp[warp] + inc - x;
+        if (k < nblk) cnt[k] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + x;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_rank_fill(const __grid_constant__ Batch b, int64_t n) {
+    __shared__ unsigned s_w[kBlock / 32];
+    const int v = blockIdx.y;
+    PartCtx c;
+    if (!b.out[v].entry_splat || !part_ctx(b, v, c)) return;
+    const Workspace &ws = b.ws[v];
+    const int64_t row = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const bool drawn = row < n && ws.rect[row].y != 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, drawn);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_w[warp] = (unsigned)__popc(bal);
+    __syncthreads();
+    unsigned pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_w[w];
+    if (drawn)
+        rank_buffer(ws)[row] = (unsigned)ws.proj_status[blockIdx.x] + pre +
+                               (unsigned)__popc(bal & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(kBlock) k_export_runs(const __grid_constant__ Batch b) {
+    const int v = blockIdx.y;
+    PartCtx c;
+    int32_t *out = b.out[v].entry_splat;
+    if (!out || !part_ctx(b, v, c)) return;
+    const Workspace &ws = b.ws[v];
+    const int64_t e = b.out[v].counters[G6R_CNT_ENTRIES];
+    const unsigned *cidx = rank_buffer(ws);
+    const unsigned *rows = ws.vals[0];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e;
+         k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = (int32_t)cidx[rows[k]];
+}
+
 static size_t scatter_smem_bytes(int tiles) {
     return (size_t)((tiles + 3) & ~3) * sizeof(unsigned) + (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
 }
@@ -312,13 +389,13 @@ int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st)
     const unsigned long long vmask = (1ull << vbits) - 1ull;
     const size_t count_smem = (size_t)kScatterWarps * ((tiles + 1) / 2) * sizeof(unsigned);
     const size_t scatter_smem = scatter_smem_bytes(tiles);
-    static bool attrs = false;
-    if (!attrs) {
+    static std::atomic<unsigned long long> attrs_done{0};   // one bit per device
+    if (const unsigned long long bit = device_bit(); !(attrs_done.load() & bit)) {
         cudaFuncSetAttribute(k_chunk_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kScatterWarps * (kMaxSplatSortTiles / 2) * sizeof(unsigned)));
         cudaFuncSetAttribute(k_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)scatter_smem_bytes(kMaxSplatSortTiles));
-        attrs = true;
+        attrs_done.fetch_or(bit);   // idempotent: a racing thread sets the same values
     }
     const dim3 cgrid((unsigned)chunks, (unsigned)b.nviews);
     k_chunk_count<<<cgrid, kBlock, count_smem, st>>>(b, vmask);
@@ -329,6 +406,17 @@ int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st)
     trace_mark("tile_scan", st);
     k_chunk_scatter<<<cgrid, kBlock, scatter_smem, st>>>(b, vmask);
     trace_mark("chunk_scatter", st);
+    bool want_runs = false;
+    for (int v = 0; v < b.nviews; ++v) want_runs = want_runs || b.out[v].entry_splat;
+    if (want_runs && n > 0) {
+        const int64_t nblk = ceil_div(n, kBlock);
+        k_rank_scan<<<dim3(1, b.nviews), 1024, 0, st>>>(b, nblk);
+        k_rank_fill<<<dim3((unsigned)nblk, b.nviews), kBlock, 0, st>>>(b, n);
+        int64_t cap = b.ws[0].entry_capacity;
+        const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, kBlock), 1184));
+        k_export_runs<<<dim3(gx, b.nviews), kBlock, 0, st>>>(b);
+        trace_mark("export_runs", st);
+    }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 

@@ -456,6 +456,17 @@ struct LossGraph {
 };
 static std::vector<LossGraph> g_loss_graphs;
 static std::mutex g_loss_mu;
+constexpr size_t kMaxLossGraphs = 8;   // bounded: callers that allocate a workspace per call evict
+
+static void destroy_graph(LossGraph &g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.in) cudaEventDestroy(g.in);
+    if (g.out) cudaEventDestroy(g.out);
+    if (g.stream) cudaStreamDestroy(g.stream);
+    g.exec = nullptr;
+    g.in = g.out = nullptr;
+    g.stream = nullptr;
+}
 
 int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, double lambda_l1,
               double lambda_ssim, int scales, const double *weights_in, void *ws, double *grad,
@@ -464,6 +475,10 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return G6R_EINVAL;
+    // one caller at a time: the graph cache, the window constants and the
+    // replay (every call ends synchronised, so no cached graph is in flight
+    // when another call evicts it)
+    std::lock_guard<std::mutex> lock(g_loss_mu);
     if (!win_set[dev]) {
         double wv[kWin];
         window_host(wv);
@@ -477,18 +492,23 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
     double *ipred = reinterpret_cast<double *>(base + L.in_pred);
     double *itgt = reinterpret_cast<double *>(base + L.in_tgt);
     double *ograd = reinterpret_cast<double *>(base + L.out_grad);
-    std::lock_guard<std::mutex> lock(g_loss_mu);   // one replay of a graph at a time
     LossGraph *gr = nullptr;
-    for (auto &g : g_loss_graphs) {
+    for (size_t k = 0; k < g_loss_graphs.size(); ++k) {
+        const LossGraph &g = g_loss_graphs[k];
         bool same = g.dev == dev && g.h == h && g.w == w && g.tc == tc && g.scales == scales &&
                     g.l1 == lambda_l1 && g.ssim == lambda_ssim && g.ws == ws;
         for (int j = 0; same && j < scales; ++j) same = g.weights[j] == weights_in[j];
-        if (same) {
-            gr = &g;
+        if (same) {   // move to the back (most recently used)
+            std::rotate(g_loss_graphs.begin() + k, g_loss_graphs.begin() + k + 1, g_loss_graphs.end());
+            gr = &g_loss_graphs.back();
             break;
         }
     }
     if (!gr) {
+        if (g_loss_graphs.size() >= kMaxLossGraphs) {   // evict the least recently used
+            destroy_graph(g_loss_graphs.front());
+            g_loss_graphs.erase(g_loss_graphs.begin());
+        }
         LossGraph g{};
         g.dev = dev;
         g.h = h;
@@ -511,7 +531,10 @@ int loss_grad(const double *pred, const double *tgt, int tc, int h, int w, doubl
                  cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess;
         }
         if (graph) cudaGraphDestroy(graph);
-        if (!ok) return G6R_ECUDA;
+        if (!ok) {
+            destroy_graph(g);
+            return G6R_ECUDA;
+        }
         g_loss_graphs.push_back(g);
         gr = &g_loss_graphs.back();
     }

@@ -380,17 +380,21 @@ def select_rows(scene, prep: ScenePrep, group_mask, config: RenderConfig,
 # Camera / config structs
 # ---------------------------------------------------------------------------
 
-def _check_config(config: RenderConfig) -> nat.Config:
-    config.dtype()
+def _check_config(config) -> nat.Config:
+    """Validate a RenderConfig -- ours, or the reference's own
+    ``splatct.raster.RenderConfig`` (no ``exp_mode``: the exact path)."""
+    if config.precision not in ("f32", "f64"):
+        raise InvalidParameterError(f"precision must be 'f32' or 'f64', got {config.precision!r}")
+    exp_mode = getattr(config, "exp_mode", "exact")
     if config.backend not in _BACKEND_NAMES:
         raise InvalidParameterError(f"unknown backend {config.backend!r}")
     if not 1 <= int(config.tile_size) <= 32:
         raise InvalidParameterError(f"tile_size must lie in [1, 32], got {config.tile_size}")
-    if config.exp_mode not in ("exact", "fast"):
-        raise InvalidParameterError(f"exp_mode must be 'exact' or 'fast', got {config.exp_mode!r}")
+    if exp_mode not in ("exact", "fast"):
+        raise InvalidParameterError(f"exp_mode must be 'exact' or 'fast', got {exp_mode!r}")
     return nat.Config(int(config.tile_size), 0 if config.precision == "f32" else 1,
                       float(config.low_pass), float(config.alpha_max),
-                      1 if config.exp_mode == "fast" else 0, 0)
+                      1 if exp_mode == "fast" else 0, 0)
 
 
 def _camera_struct(camera) -> nat.Camera:
@@ -526,7 +530,7 @@ PIPELINE_LANES = int(os.environ.get("G6R_LANES", "2"))   # streams batches alter
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
                  capacity: int | None = None, out=None, profiler=None,
                  concurrency: int = DEFAULT_CONCURRENCY, rgba8=None, background=(0.0, 0.0, 0.0),
-                 image: bool = True, pipeline: bool = True):
+                 image: bool = True, pipeline: bool = True, entry_splat=None, tile_starts=None):
     """Render ``cameras`` (same size) with up to ``concurrency`` views in flight.
 
     Returns ``(images, counters)``: ``images`` (V,H,W,4) on the device,
@@ -535,7 +539,12 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     ``rgba8`` ((V,H,W,4) uint8 device tensor) additionally receives the served
     frame composited over ``background`` and quantised in the compositor's
     epilogue; with ``image=False`` the float image is not written at all
-    (``images`` is then None)."""
+    (``images`` is then None).
+    ``entry_splat`` ((V, capacity) int32) and ``tile_starts`` ((V, T+1) int64)
+    device tensors, when given, receive every view's sorted tile runs exactly
+    as ``TileEntries`` holds them (indices into the view's compacted
+    SplatBatch, raster.py:201-208); entries past ``counters[v, 1]`` are
+    undefined."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cfg = _check_config(config)
@@ -557,6 +566,14 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         raise InvalidParameterError(f"rgba8 must be a contiguous ({V}, {H}, {W}, 4) uint8 tensor")
     counters = torch.empty((V, nat.NCOUNTERS), dtype=torch.int64, device=dev)
     cap = int(capacity or prep.entry_hint)
+    T = (lambda t: t[0] * t[1])(_tiles(cams[0], cfg.tile_size))
+    if entry_splat is not None and (entry_splat.dtype != torch.int32 or not entry_splat.is_contiguous()
+                                    or entry_splat.dim() != 2 or entry_splat.shape[0] != V
+                                    or entry_splat.shape[1] < cap):
+        raise InvalidParameterError(f"entry_splat must be a contiguous (V, >= {cap}) int32 tensor")
+    if tile_starts is not None and (tile_starts.dtype != torch.int64 or not tile_starts.is_contiguous()
+                                    or tuple(tile_starts.shape) != (V, T + 1)):
+        raise InvalidParameterError(f"tile_starts must be a contiguous ({V}, {T + 1}) int64 tensor")
     slots = max(1, min(int(concurrency), MAX_BATCH, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
@@ -566,7 +583,9 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
     bg = (ctypes.c_double * 3)(*[float(c) for c in background])
     frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr() if images is not None else 0, 0, 0,
-                                         counters[v].data_ptr(), 0, 0,
+                                         counters[v].data_ptr(),
+                                         entry_splat[v].data_ptr() if entry_splat is not None else 0,
+                                         tile_starts[v].data_ptr() if tile_starts is not None else 0,
                                          rgba8[v].data_ptr() if rgba8 is not None else 0, bg)
                                for v in range(V)])
     sc = prep.scene_struct()
@@ -576,6 +595,19 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
                                           _stream_handle()))
     counters._g6r_keepalive = ws
     return images, counters
+
+
+def _balanced_slices(V: int, chunk: int):
+    """Split V views into ceil(V / chunk) contiguous slices of (almost) equal
+    size: 20 views at 16 become 10 + 10 instead of 16 + a 4-view tail."""
+    nb = max(1, -(-V // max(1, chunk)))
+    base, extra = divmod(V, nb)
+    out, k = [], 0
+    for i in range(nb):
+        step = base + (1 if i < extra else 0)
+        out.append(slice(k, k + step))
+        k += step
+    return out
 
 
 _LANES = {}
@@ -621,8 +653,7 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         ln.wait_stream(main)
     counters = []
     chunk = max(1, min(int(batch), MAX_BATCH))
-    for i, k in enumerate(range(0, V, chunk)):
-        sl = slice(k, min(V, k + chunk))
+    for i, sl in enumerate(_balanced_slices(V, chunk)):
         lane = lanes[i & 1]
         with torch.cuda.stream(lane):
             _, cnt = render_views(scene, cams[sl], group_mask, config, out=images[sl],
@@ -667,8 +698,7 @@ def render_frames_u8(scene, cameras, background=(0.0, 0.0, 0.0), group_mask=None
     main = torch.cuda.current_stream()
     copy = torch.cuda.Stream(device=dev)
     counters = []
-    for k in range(0, V, chunk):
-        sl = slice(k, min(V, k + chunk))
+    for sl in _balanced_slices(V, chunk):
         _, cnt = render_views(scene, cams[sl], group_mask, config, concurrency=chunk,
                               rgba8=frames[sl], background=background, image=False)
         counters.append(cnt)

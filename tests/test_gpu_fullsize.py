@@ -12,6 +12,7 @@ import torch
 from paper_2505_17338_b200 import raster, scenes
 from paper_2505_17338_b200.raster import RenderConfig
 
+from test_gpu_hotpath_runs import hot_runs
 from test_gpu_parity import assert_image_close
 
 pytestmark = pytest.mark.gpu
@@ -34,12 +35,13 @@ def test_full_size_view_matches_oracle(oracle, scene1m, size, count, view):
     np.testing.assert_array_equal(st.image, want.image)
     np.testing.assert_array_equal(st.last_contrib, want.last_contrib)
     np.testing.assert_array_equal(st.final_t, want.final_t)
-    imgs, cnt = raster.render_views(scene1m, [cam, cam])
-    torch.cuda.synchronize()
-    c = cnt.cpu().numpy()
+    # the benchmarked path: splat sort + tile partition, runs exported
+    imgs, c, runs = hot_runs(scene1m, [cam, cam])
     assert int(c[:, 8].sum()) == 0
     assert tuple(c[0, :2]) == (st.stats.n_drawn, st.stats.n_entries)
     for k in range(2):
+        np.testing.assert_array_equal(runs[k][1], want.entries.tile_starts)
+        np.testing.assert_array_equal(runs[k][0], want.entries.entry_splat)
         np.testing.assert_array_equal(imgs[k].cpu().numpy(), want.image)
     fast, _ = raster.render_views(scene1m, [cam], config=RenderConfig(exp_mode="fast"))
     assert_image_close(fast[0].cpu().numpy(), want.image)
