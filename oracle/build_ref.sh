@@ -16,4 +16,7 @@ CC=/usr/bin/gcc LDSHARED="/usr/bin/gcc -shared" \
   python -m pip install -q --no-index --no-build-isolation --no-deps \
   --find-links /opt/wheelhouse --target "$HERE/_ref" "$TMP/pkg"
 rm -rf "$TMP"
+# the reference's own test suite, unmodified, so the GPU box can run it against
+# the B200 path through paper_2505_17338_b200.integrate (tests/test_gpu_integrate.py)
+cp -r "$SRC/tests" "$HERE/_ref/ref_tests"
 echo "reference built into $HERE/_ref"

@@ -42,7 +42,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_counts, rect, chunk_hist, warp_prefix, tile_total, total;
+        sort_counts, rect, chunk_hist, warp_prefix, tile_total, sched, total;
     int64_t sort_tiles_cap;
 };
 
@@ -84,6 +84,8 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
                          sizeof(unsigned));
     L.tile_total = o;
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
+    L.sched = o;   // compositor work order (this view's slice of the batch's ranking)
+    o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -105,6 +107,7 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.chunk_hist = reinterpret_cast<unsigned *>(b + L.chunk_hist);
     w.warp_prefix = reinterpret_cast<unsigned *>(b + L.warp_prefix);
     w.tile_total = reinterpret_cast<unsigned *>(b + L.tile_total);
+    w.sched = reinterpret_cast<unsigned *>(b + L.sched);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;
     return w;

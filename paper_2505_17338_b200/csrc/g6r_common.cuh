@@ -31,6 +31,7 @@ enum {
     kDepthMax = 11,        // max f32 depth bits
     kValsBuffer = 9,       // which vals buffer holds the sorted entry values
     kSortPasses = 12,      // radix passes actually needed (decided on the device)
+    kTicketComposite = 13, // compositor work-item ticket (slot of the batch's first view)
     kNumInternal = 16
 };
 

@@ -193,10 +193,31 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
 template <typename Real, int kNB, int kSub = 1, bool kFastExp = false>
-__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024)
-k_composite(const __grid_constant__ Batch bt, int sorted) {
+__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024, (kNB == 128 && sizeof(Real) == 4) ? 10 : 1)
+k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
     using S = typename Px<Real>::S;
-    const int view = blockIdx.y;
+    // Work item: with `scheduled` (kSub > 1), CTAs take (view, tile) items in
+    // k_sched_order's longest-run-first order through a ticket, both bands of
+    // a tile back to back, so the batch's heaviest runs start first and the
+    // launch's tail is made of short ones; otherwise blockIdx names the item.
+    __shared__ unsigned s_item;
+    int view, item_x;
+    if (kSub > 1 && scheduled) {
+        if (threadIdx.x == 0) {
+            const unsigned k = (unsigned)atomicAdd(
+                reinterpret_cast<unsigned long long *>(&bt.ws[0].internal[kTicketComposite]), 1ull);
+            const int T = bt.vp[0].tiles_x * bt.vp[0].tiles_y;
+            const unsigned r = k / kSub;
+            const unsigned it = bt.ws[r / T].sched[r % T];
+            s_item = ((it >> 16) << 16) | ((it & 0xffffu) * kSub + k % kSub);
+        }
+        __syncthreads();
+        view = (int)(s_item >> 16);
+        item_x = (int)(s_item & 0xffffu);
+    } else {
+        view = blockIdx.y;
+        item_x = blockIdx.x;
+    }
     const ViewParams &vp = bt.vp[view];
     const Workspace &wsv = bt.ws[view];
     const typename Px<Real>::Payload *__restrict__ payload =
@@ -222,8 +243,8 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     // kSub > 1 (16x16 tiles only): the tile's rows are split over kSub CTAs,
     // each walking the whole run for its band, so a band that saturates early
     // frees its SM slot instead of idling at the other band's barriers
-    const int tile = kSub > 1 ? (int)(blockIdx.x / kSub) : (int)blockIdx.x;
-    const int band = kSub > 1 ? (int)(blockIdx.x % kSub) * (16 / kSub) : 0;
+    const int tile = kSub > 1 ? item_x / kSub : item_x;
+    const int band = kSub > 1 ? (item_x % kSub) * (16 / kSub) : 0;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
     int ox, oy;
     tile_pixel(ts, threadIdx.x, ox, oy);
@@ -375,6 +396,51 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     }
 }
 
+// Compositor work order for a batch: every (view, tile) item ranked by its run
+// length, longest first (quarter-octave buckets; order inside a bucket is
+// arbitrary -- no pixel depends on which CTA composites it or when).  One CTA:
+// bucket histogram in shared memory, scan, scatter.  Rank r of the batch lives
+// at ws[r / T].sched[r % T]; the compositor's ticket (first view's internal
+// slot) is reset here, so the launch needs no cleared workspace.
+constexpr int kSchedBuckets = 128;
+__device__ __forceinline__ int sched_bucket(int64_t len) {
+    if (len <= 0) return kSchedBuckets - 1;   // empty runs last
+    const float l2 = __log2f((float)len + 1.0f);
+    const int q = (int)(l2 * 4.0f);           // 4 buckets per octave
+    return max(0, kSchedBuckets - 2 - q);     // longer -> earlier
+}
+
+__global__ void __launch_bounds__(1024) k_sched_order(const __grid_constant__ Batch bt) {
+    __shared__ unsigned s_cnt[kSchedBuckets];
+    const int T = bt.vp[0].tiles_x * bt.vp[0].tiles_y;
+    const int total = T * bt.nviews;
+    for (int k = threadIdx.x; k < kSchedBuckets; k += blockDim.x) s_cnt[k] = 0;
+    if (threadIdx.x == 0) bt.ws[0].internal[kTicketComposite] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int64_t *st = bt.ws[i / T].tile_starts;
+        const int t = i % T;
+        atomicAdd(&s_cnt[sched_bucket(st[t + 1] - st[t])], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the buckets, one warp
+        unsigned carry = 0;
+        for (int b0 = 0; b0 < kSchedBuckets; b0 += 32) {
+            const unsigned x = s_cnt[b0 + threadIdx.x];
+            const unsigned inc = warp_inclusive_scan(x);
+            s_cnt[b0 + threadIdx.x] = carry + inc - x;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int v = i / T, t = i % T;
+        const int64_t *st = bt.ws[v].tile_starts;
+        const unsigned r = atomicAdd(&s_cnt[sched_bucket(st[t + 1] - st[t])], 1u);
+        bt.ws[r / T].sched[r % T] = ((unsigned)v << 16) | (unsigned)t;
+    }
+}
+
 // Pack reference-shaped splat arrays (raster.py:405-408) into payloads.
 template <typename Real>
 __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conics, const Real *colors,
@@ -501,6 +567,14 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     const dim3 grid((unsigned)(vp.tiles_x * vp.tiles_y), (unsigned)b.nviews);
     if (grid.x == 0) return G6R_OK;
     const int srt = sorted ? 1 : 0;
+    // longest-run-first work order (16x16 tiles: the kSub band kernels)
+    bool sched = vp.tile_size == 16 && grid.x * kCompositeSub <= 65535;
+    for (int v = 0; v < b.nviews; ++v) sched = sched && b.ws[v].sched && b.ws[v].internal;
+    if (sched) {
+        k_sched_order<<<1, 1024, 0, st>>>(b);
+        trace_mark("sched_order", st);
+    }
+    const int sc = sched ? 1 : 0;
     // > 48 KB dynamic smem for large f64 tiles; the attribute is per device
     static std::atomic<unsigned long long> attrs_done{0};
     if (const unsigned long long bit = device_bit(); !(attrs_done.load() & bit)) {
@@ -513,20 +587,20 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     if (vp.precision) {
         if (vp.tile_size == 16)
             k_composite<double, 256 / kCompositeSub, kCompositeSub>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
         else
-            k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
+            k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt, 0);
     } else {
         bool fast = vp.exp_mode == 1;
         for (int v = 0; v < b.nviews; ++v) fast = fast && !b.out[v].rgba8;   // served bytes stay exact
         if (vp.tile_size == 16 && fast)
             k_composite<float, 256 / kCompositeSub, kCompositeSub, true>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
         else if (vp.tile_size == 16)
             k_composite<float, 256 / kCompositeSub, kCompositeSub>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
         else
-            k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
+            k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt, 0);
     }
     trace_mark("composite", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;

@@ -31,6 +31,7 @@ struct Workspace {
     unsigned *chunk_hist;           // splat-sort path: per chunk of sorted splats, T tile counts
     unsigned *warp_prefix;          // splat-sort path: per chunk, per scatter warp, packed u16 tile offsets
     unsigned *tile_total;           // splat-sort path: T entry counts
+    unsigned *sched;                // T: compositor work items, longest run first (k_sched_order)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
 };
