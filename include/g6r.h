@@ -329,6 +329,10 @@ int g6r_trace_dump(const char *path);
  * algorithm, g6r_common.cuh) for n floats. */
 int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream);
 
+/* Test probe: y[i] = the device exp used by the f64 compositors (glibc 2.39's
+ * FMA exp restated, g6r_common.cuh exp_glibc) for n doubles in (-512, 512). */
+int g6r_debug_exp(int64_t n, const double *x, double *y, g6r_stream_t stream);
+
 /* Stage entry points with external inputs (the reference stage helpers). */
 int g6r_project(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
                 const g6r_config *cfg, void *workspace, size_t workspace_bytes,

@@ -264,6 +264,14 @@ float or_expf_glibc(float x)
     return (float)y;
 }
 
+/* The host libm exp over an array (checker for the device's restated glibc
+ * exp used by the f64 compositors; the reference's f64 kernel and its
+ * brute-force oracle call this same libm exp). */
+void or_libm_exp_batch(int64_t n, const double *x, double *y)
+{
+    for (int64_t i = 0; i < n; ++i) y[i] = exp(x[i]);
+}
+
 void or_expf_glibc_batch(int64_t n, const float *x, float *y)
 {
     for (int64_t i = 0; i < n; ++i) y[i] = or_expf_glibc(x[i]);

@@ -66,6 +66,7 @@ def lib():
             getattr(L, name).argtypes = [P, P, P, P, P, P, I64, I, I, I, I, P, P, P]
         L.or_composite_backward.argtypes = [P, P, P, P, P, P, I64, I, I, I, I, P, P, P, P]
         L.or_expf_glibc_batch.argtypes = [I64, P, P]
+        L.or_libm_exp_batch.argtypes = [I64, P, P]
         L.or_fma_batch.argtypes = [I64, P, P, P, P]
         _lib = L
     return _lib
@@ -336,9 +337,10 @@ def composite(means2d, conics, colors, alphas, entry_splat, tile_starts, tiles_x
 
 
 def composite_backward(means2d, conics, colors, alphas, entry_splat, tile_starts, tiles_x,
-                       tile_size, width, height, final_t, last_contrib, grad_image):
+                       tile_size, width, height, final_t, last_contrib, grad_image, init=0.0):
+    """Per-entry gradient rows accumulated (+=) into rows filled with `init`."""
     e = len(entry_splat)
-    grads = np.zeros((e, 9))
+    grads = np.full((e, 9), float(init))
     args = [_c(means2d, np.float64), _c(conics, np.float64), _c(colors, np.float64),
             _c(alphas, np.float64), _c(entry_splat, np.int32), _c(tile_starts, np.int64)]
     tail = [_c(final_t, np.float64), _c(last_contrib, np.int32), _c(grad_image, np.float64)]
@@ -375,6 +377,14 @@ def render_with_state(scene, camera, group_mask=None, precision="f32", w_mode="p
 
 def render(scene, camera, group_mask=None, precision="f32", **kw):
     return render_with_state(scene, camera, group_mask, precision, **kw).image
+
+
+def libm_exp(x):
+    """The host libm exp (glibc 2.39) over a float64 array."""
+    x = _c(x, np.float64)
+    y = np.empty_like(x)
+    lib().or_libm_exp_batch(x.size, _p(x), _p(y))
+    return y
 
 
 def expf_glibc(x):

@@ -742,6 +742,12 @@ int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream) {
     return G6R_OK;
 }
 
+int g6r_debug_exp(int64_t n, const double *x, double *y, g6r_stream_t stream) {
+    if (n < 0) return fail(G6R_EINVAL, "n must be >= 0");
+    if (launch_debug_exp(n, x, y, (cudaStream_t)stream)) return cuda_check("debug_exp");
+    return G6R_OK;
+}
+
 int g6r_project(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *cam,
                 const g6r_config *cfg, void *workspace, size_t workspace_bytes,
                 int64_t *counters, const g6r_splat_out *splats, g6r_stream_t stream) {

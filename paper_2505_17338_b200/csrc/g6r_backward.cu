@@ -31,6 +31,8 @@ struct BwdSplat {
 // Two CTAs per tile, one per 16x8 band (8x4 warp blocks, as the forward), one
 // thread per pixel; each band sweeps the run back to front from its own largest
 // last_contrib and writes its own row per entry (egrad + band * cap * 9).
+__constant__ unsigned long long c_bwd_exp_tab[256] = G6R_EXP_TABLE;
+
 __global__ void __launch_bounds__(128)
 k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                 const unsigned *vals0, const unsigned *vals1, const long long *internal,
@@ -45,6 +47,8 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
     __shared__ unsigned char s_hit[4][kBwdBatch];
     __shared__ float4 s_wbox[4];
     __shared__ int s_maxlast;
+    __shared__ unsigned long long s_etab[256];   // glibc exp table (g6r_common.cuh)
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) s_etab[k] = c_bwd_exp_tab[k];
     const int ts = 16;
     const int tile = blockIdx.x >> 1, band = (int)(blockIdx.x & 1) * 8;
     double *__restrict__ egrad = egrad_all + (int64_t)(blockIdx.x & 1) * cap * 9;
@@ -116,7 +120,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                 const double dx = fx - s.mx, dy = fy - s.my;
                 const double pw = -0.5 * (s.ca * dx * dx + s.cc * dy * dy) - s.cb * dx * dy;
                 if (!(pw > 0.0 || pw < -4.5)) {
-                    const double ge = exp(pw);
+                    const double ge = exp_glibc(pw, s_etab);   // libm exp (_kernels.pyx:172)
                     const double ai = s.alpha * ge;
                     if (!(ai < 1.0 / 255.0)) {
                         const double om = 1.0 - ai;

@@ -12,6 +12,7 @@
 // framebuffer matches the reference's bit for bit.  Nothing here is a dense
 // contraction, so it runs on the FP32/FP64 pipes, not tensor cores.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 #include "g6r_common.cuh"
@@ -20,6 +21,7 @@
 namespace g6r {
 
 __constant__ unsigned long long c_expf_tab[32] = G6R_EXPF_TABLE;
+__constant__ unsigned long long c_exp_tab[256] = G6R_EXP_TABLE;   // f64 glibc exp
 
 template <typename Real>
 struct Px;
@@ -234,8 +236,11 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
     S *sp = kNB > 0 ? s_sp_static : reinterpret_cast<S *>(smem_raw);
     unsigned *smask = kNB > 0 ? s_mask_static : reinterpret_cast<unsigned *>(sp + 2 * nb);
     __shared__ unsigned long long s_tab[32];
+    __shared__ unsigned long long s_tab64[sizeof(Real) == 8 ? 256 : 1];
     __shared__ float4 s_wbox[32];   // pixel-centre box per warp
     for (int k = threadIdx.x; k < 32; k += blockDim.x) s_tab[k] = c_expf_tab[k];   // tiles below 6x6 have < 32 threads
+    if constexpr (sizeof(Real) == 8)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab64[k] = c_exp_tab[k];
     const uint32_t sp_base = smem_addr(sp), mask_base = smem_addr(smask);
     const ExpOperands eops = exp_operands(smem_addr(s_tab));
 
@@ -349,6 +354,8 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
                         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
                         ai = al * e;
                         if (fabsf(ai - floor_a) <= 2e-6f * floor_a) ai = al * splat_exp_s(pw, eops);
+                    } else if constexpr (sizeof(Real) == 8) {
+                        ai = al * exp_glibc(pw, s_tab64);   // libm exp, bit for bit
                     } else {
                         ai = al * splat_exp_s(pw, eops);
                     }
@@ -468,63 +475,105 @@ __global__ void k_pack_payload(int64_t m, const Real *means2d, const Real *conic
     }
 }
 
-// Adjoint (f64), one thread per pixel, reverse sweep from last_contrib with
-// the running transmittance rebuilt by division (_kernels.pyx:135-187).  Each
-// pixel adds into the rows of the entries it touched; entries are shared by
-// the pixels of one tile only, so the adds are CTA-local shared-memory-free
-// atomics on distinct (entry, slot) addresses.
-__global__ void k_composite_backward(ViewParams vp, const double *__restrict__ means2d,
-                                     const double *__restrict__ conics, const double *__restrict__ colors,
-                                     const double *__restrict__ alphas, const int32_t *__restrict__ entry_splat,
-                                     const int64_t *__restrict__ starts, const double *__restrict__ final_t,
-                                     const int32_t *__restrict__ last_contrib,
-                                     const double *__restrict__ grad_image, double *entry_grads) {
+// Adjoint (f64) of the kernel-module contract (_kernels.pyx:108-187): per-entry
+// gradient rows accumulated (+=) into the caller's entry_grads.  One CTA per
+// tile, one thread per pixel, row-major (the reference's py-outer, px-inner
+// loop).  The CTA walks the tile's entries back to front in lock step; each
+// pixel keeps its own reverse sweep (T rebuilt by division, suffix sums) and
+// contributes to entry e only while e < its last_contrib.  The contributions
+// to one entry are then added in pixel order by 9 reducer threads (one per
+// gradient slot), skipping pixels that did not contribute -- the reference's
+// summation order, so the rows are deterministic and bit-identical to it (no
+// floating-point atomics).
+__global__ void __launch_bounds__(1024)
+k_composite_backward(ViewParams vp, const double *__restrict__ means2d,
+                     const double *__restrict__ conics, const double *__restrict__ colors,
+                     const double *__restrict__ alphas, const int32_t *__restrict__ entry_splat,
+                     const int64_t *__restrict__ starts, const double *__restrict__ final_t,
+                     const int32_t *__restrict__ last_contrib,
+                     const double *__restrict__ grad_image, double *entry_grads,
+                     const unsigned long long *__restrict__ exp_tab) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
     const int ts = vp.tile_size;
+    const int npix = ts * ts;
+    double *s_c = reinterpret_cast<double *>(s_raw);                       // [9][npix]
+    unsigned char *s_f = reinterpret_cast<unsigned char *>(s_c + 9 * npix);   // [npix]
+    __shared__ unsigned long long s_tab[256];
+    __shared__ int s_maxlast;
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = exp_tab[k];
+    if (threadIdx.x == 0) s_maxlast = 0;
     const int tile = blockIdx.x;
-    const int px = (tile % vp.tiles_x) * ts + (int)threadIdx.x % ts;
-    const int py = (tile / vp.tiles_x) * ts + (int)threadIdx.x / ts;
-    if (px >= vp.iw || py >= vp.ih) return;
-    const int64_t p = (int64_t)py * vp.iw + px;
-    const int last = last_contrib[p];
-    if (last == 0) return;
-    const double gr = grad_image[4 * p], gg = grad_image[4 * p + 1];
-    const double gb = grad_image[4 * p + 2], ga = grad_image[4 * p + 3];
-    if (gr == 0.0 && gg == 0.0 && gb == 0.0 && ga == 0.0) return;
+    const int t = threadIdx.x;
+    const int px = (tile % vp.tiles_x) * ts + t % ts;
+    const int py = (tile / vp.tiles_x) * ts + t / ts;
+    const bool inside = px < vp.iw && py < vp.ih;
+    int last = 0;
+    double gr = 0.0, gg = 0.0, gb = 0.0, ga = 0.0, T = 1.0;
+    if (inside) {
+        const int64_t p = (int64_t)py * vp.iw + px;
+        last = last_contrib[p];
+        gr = grad_image[4 * p];
+        gg = grad_image[4 * p + 1];
+        gb = grad_image[4 * p + 2];
+        ga = grad_image[4 * p + 3];
+        T = final_t[p];
+        if (gr == 0.0 && gg == 0.0 && gb == 0.0 && ga == 0.0) last = 0;
+    }
+    __syncthreads();
+    if (last > 0) atomicMax(&s_maxlast, last);
+    __syncthreads();
     const int64_t lo = starts[tile];
     const double fx = (double)px, fy = (double)py;
-    double T = final_t[p];
     double sr = 0.0, sg = 0.0, sb = 0.0, sa = 0.0;
-    for (int64_t e = lo + last - 1; e >= lo; --e) {
-        const int64_t s = entry_splat[e];
-        const double dx = fx - means2d[2 * s];
-        const double dy = fy - means2d[2 * s + 1];
-        const double qa = conics[3 * s], qb = conics[3 * s + 1], qc = conics[3 * s + 2];
-        const double pw = -0.5 * (qa * dx * dx + qc * dy * dy) - qb * dx * dy;
-        if (pw > 0.0 || pw < -4.5) continue;
-        const double ge = exp(pw);
-        const double ai = alphas[s] * ge;
-        if (ai < 1.0 / 255.0) continue;
-        const double om = 1.0 - ai;
-        T = T / om;
-        const double w = ai * T;
-        const double *col = colors + 3 * s;
-        double *eg = entry_grads + 9 * e;
-        atomicAdd(eg + 5, w * gr);
-        atomicAdd(eg + 6, w * gg);
-        atomicAdd(eg + 7, w * gb);
-        const double dai = T * (col[0] * gr + col[1] * gg + col[2] * gb + ga) -
-                           (sr * gr + sg * gg + sb * gb + sa * ga) / om;
-        atomicAdd(eg + 8, ge * dai);
-        const double dp = ai * dai;
-        atomicAdd(eg + 0, dp * (qa * dx + qb * dy));
-        atomicAdd(eg + 1, dp * (qc * dy + qb * dx));
-        atomicAdd(eg + 2, dp * (-0.5 * dx * dx));
-        atomicAdd(eg + 3, dp * (-dx * dy));
-        atomicAdd(eg + 4, dp * (-0.5 * dy * dy));
-        sr = sr + col[0] * w;
-        sg = sg + col[1] * w;
-        sb = sb + col[2] * w;
-        sa = sa + w;
+    for (int64_t e = lo + s_maxlast - 1; e >= lo; --e) {
+        double c[9];
+        bool contrib = false;
+        if (e < lo + last) {
+            const int64_t s = entry_splat[e];
+            const double dx = fx - means2d[2 * s];
+            const double dy = fy - means2d[2 * s + 1];
+            const double qa = conics[3 * s], qb = conics[3 * s + 1], qc = conics[3 * s + 2];
+            const double pw = -0.5 * (qa * dx * dx + qc * dy * dy) - qb * dx * dy;
+            if (!(pw > 0.0 || pw < -4.5)) {
+                const double ge = exp_glibc(pw, s_tab);
+                const double ai = alphas[s] * ge;
+                if (!(ai < 1.0 / 255.0)) {
+                    const double om = 1.0 - ai;
+                    T = T / om;
+                    const double w = ai * T;
+                    const double *col = colors + 3 * s;
+                    c[5] = w * gr;
+                    c[6] = w * gg;
+                    c[7] = w * gb;
+                    const double dai = T * (col[0] * gr + col[1] * gg + col[2] * gb + ga) -
+                                       (sr * gr + sg * gg + sb * gb + sa * ga) / om;
+                    c[8] = ge * dai;
+                    const double dp = ai * dai;
+                    c[0] = dp * (qa * dx + qb * dy);
+                    c[1] = dp * (qc * dy + qb * dx);
+                    c[2] = dp * (-0.5 * dx * dx);
+                    c[3] = dp * (-dx * dy);
+                    c[4] = dp * (-0.5 * dy * dy);
+                    sr = sr + col[0] * w;
+                    sg = sg + col[1] * w;
+                    sb = sb + col[2] * w;
+                    sa = sa + w;
+                    contrib = true;
+                }
+            }
+        }
+        s_f[t] = contrib ? 1 : 0;
+        if (contrib)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) s_c[k * npix + t] = c[k];
+        __syncthreads();
+        if (t < 9) {   // slot t of entry e: the pixels' terms in row-major order
+            double acc = entry_grads[9 * e + t];
+            for (int q = 0; q < npix; ++q)
+                if (s_f[q]) acc = acc + s_c[t * npix + q];
+            entry_grads[9 * e + t] = acc;
+        }
+        __syncthreads();
     }
 }
 
@@ -535,6 +584,21 @@ __global__ void k_debug_expf(int64_t n, const float *x, float *y) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         y[i] = expf_glibc(x[i], s_tab);
+}
+
+__global__ void k_debug_exp(int64_t n, const double *x, double *y) {
+    __shared__ unsigned long long s_tab[256];
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = c_exp_tab[k];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = exp_glibc(x[i], s_tab);
+}
+
+int launch_debug_exp(int64_t n, const double *x, double *y, cudaStream_t st) {
+    if (n == 0) return G6R_OK;
+    k_debug_exp<<<(unsigned)std::min<int64_t>(ceil_div(n, kBlock), 148 * 16), kBlock, 0, st>>>(n, x, y);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st) {
@@ -568,7 +632,11 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     if (grid.x == 0) return G6R_OK;
     const int srt = sorted ? 1 : 0;
     // longest-run-first work order (16x16 tiles: the kSub band kernels)
-    bool sched = vp.tile_size == 16 && grid.x * kCompositeSub <= 65535;
+    static const int sched_env = [] {   // G6R_SCHED=0 keeps launch order (A/B probe)
+        const char *e = getenv("G6R_SCHED");
+        return e ? atoi(e) : 1;
+    }();
+    bool sched = sched_env && vp.tile_size == 16 && grid.x * kCompositeSub <= 65535;
     for (int v = 0; v < b.nviews; ++v) sched = sched && b.ws[v].sched && b.ws[v].internal;
     if (sched) {
         k_sched_order<<<1, 1024, 0, st>>>(b);
@@ -616,9 +684,18 @@ int launch_composite_backward(int64_t m, const double *means2d, const double *co
     const int threads = vp.tile_size * vp.tile_size;
     const unsigned grid = (unsigned)(vp.tiles_x * vp.tiles_y);
     if (grid == 0) return G6R_OK;
-    k_composite_backward<<<grid, threads, 0, st>>>(vp, means2d, conics, colors, alphas, entry_splat,
-                                                   tile_starts, final_t, last_contrib, grad_image,
-                                                   entry_grads);
+    const size_t smem = (size_t)threads * (9 * sizeof(double) + 1);
+    static std::atomic<unsigned long long> attrs_done{0};
+    if (const unsigned long long bit = device_bit(); !(attrs_done.load() & bit)) {
+        cudaFuncSetAttribute(k_composite_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(1024 * (9 * sizeof(double) + 1)));
+        attrs_done.fetch_or(bit);
+    }
+    const unsigned long long *tab = nullptr;
+    if (cudaGetSymbolAddress((void **)&tab, c_exp_tab) != cudaSuccess) return G6R_ECUDA;
+    k_composite_backward<<<grid, threads, smem, st>>>(vp, means2d, conics, colors, alphas, entry_splat,
+                                                      tile_starts, final_t, last_contrib, grad_image,
+                                                      entry_grads, tab);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
 

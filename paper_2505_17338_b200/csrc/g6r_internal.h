@@ -112,6 +112,7 @@ bool splat_sort_applies(const Batch &b);
 int launch_splat_sort(const Batch &b, int64_t n, cudaStream_t st);
 int launch_tile_partition(const Batch &b, int64_t n, int vbits, cudaStream_t st);
 int launch_debug_expf(int64_t n, const float *x, float *y, cudaStream_t st);
+int launch_debug_exp(int64_t n, const double *x, double *y, cudaStream_t st);
 int launch_pack_payload(int64_t m, int precision, const void *means2d, const void *conics,
                         const void *colors, const void *alphas, void *payload, cudaStream_t st);
 // sorted: entry values are the view's sorted ping-pong buffer; otherwise vals[0] holds them
