@@ -20,6 +20,10 @@
 
 namespace g6r {
 
+#ifndef G6R_SCHED_MINB
+#define G6R_SCHED_MINB 0   // min CTAs/SM for the scheduled f32 compositor (A/B knob)
+#endif
+
 __constant__ unsigned long long c_expf_tab[32] = G6R_EXPF_TABLE;
 __constant__ unsigned long long c_exp_tab[256] = G6R_EXP_TABLE;   // f64 glibc exp
 
@@ -194,16 +198,16 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // warp's pixel block; warps then ballot over the batch and visit only splats
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
-template <typename Real, int kNB, int kSub = 1, bool kFastExp = false>
-__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024, (kNB == 128 && sizeof(Real) == 4) ? 10 : 1)
-k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
+template <typename Real, int kNB, int kSub = 1, bool kFastExp = false, bool kSched = false>
+__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024, (kSched && sizeof(Real) == 4) ? G6R_SCHED_MINB : 0)
+k_composite(const __grid_constant__ Batch bt, int sorted) {
+    constexpr bool scheduled = kSched && kSub > 1;
     using S = typename Px<Real>::S;
     // Work item: with `scheduled` (kSub > 1), CTAs take (view, tile) items in
     // k_sched_order's longest-run-first order through a ticket, both bands of
     // a tile back to back, so the batch's heaviest runs start first and the
     // launch's tail is made of short ones; otherwise blockIdx names the item.
     __shared__ unsigned s_item;
-    int view, item_x;
     if (kSub > 1 && scheduled) {
         if (threadIdx.x == 0) {
             const unsigned k = (unsigned)atomicAdd(
@@ -214,20 +218,50 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
             s_item = ((it >> 16) << 16) | ((it & 0xffffu) * kSub + k % kSub);
         }
         __syncthreads();
-        view = (int)(s_item >> 16);
-        item_x = (int)(s_item & 0xffffu);
-    } else {
-        view = blockIdx.y;
-        item_x = blockIdx.x;
     }
+    // This thread's (view, pixel).  Derived from blockIdx or from the shared
+    // work item, and derived again in the epilogue instead of being kept: the
+    // view index and pixel coordinates then hold no registers across the
+    // compositing loop (with the scheduled item they could not be
+    // rematerialised from special registers).
+    struct Where {
+        int view, tile, band, px, py;
+        bool inside;
+    };
+    auto where = [&]() {
+        Where w;
+        int item_x;
+        if (kSub > 1 && scheduled) {
+            unsigned it;
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(it) : "r"(smem_addr(&s_item)));
+            w.view = (int)(it >> 16);
+            item_x = (int)(it & 0xffffu);
+        } else {
+            w.view = blockIdx.y;
+            item_x = blockIdx.x;
+        }
+        const ViewParams &v = bt.vp[w.view];
+        const int ts_ = v.tile_size;
+        // kSub > 1 (16x16 tiles only): the tile's rows are split over kSub
+        // CTAs, each walking the whole run for its band, so a band that
+        // saturates early frees its SM slot instead of idling at the other
+        // band's barriers
+        w.tile = kSub > 1 ? item_x / kSub : item_x;
+        w.band = kSub > 1 ? (item_x % kSub) * (16 / kSub) : 0;
+        int ox, oy;
+        tile_pixel(ts_, threadIdx.x, ox, oy);
+        w.px = (w.tile % v.tiles_x) * ts_ + ox;
+        w.py = (w.tile / v.tiles_x) * ts_ + oy + w.band;
+        w.inside = w.px < v.iw && w.py < v.ih;
+        return w;
+    };
+    const Where at = where();
+    const int view = at.view;
     const ViewParams &vp = bt.vp[view];
     const Workspace &wsv = bt.ws[view];
     const typename Px<Real>::Payload *__restrict__ payload =
         static_cast<const typename Px<Real>::Payload *>(wsv.payload);
     const int64_t *__restrict__ starts = wsv.tile_starts;
-    Real *__restrict__ image = static_cast<Real *>(bt.out[view].image);
-    Real *__restrict__ final_t = static_cast<Real *>(bt.out[view].final_t);
-    int32_t *__restrict__ last_contrib = bt.out[view].last_contrib;
     constexpr int kStatic = kNB > 0 ? kNB : 1;
     __shared__ S s_sp_static[kNB > 0 ? 2 * kStatic : 1];
     __shared__ unsigned s_mask_static[kNB > 0 ? 2 * kStatic : 1];
@@ -245,18 +279,9 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
     const ExpOperands eops = exp_operands(smem_addr(s_tab));
 
     const int ts = vp.tile_size;
-    // kSub > 1 (16x16 tiles only): the tile's rows are split over kSub CTAs,
-    // each walking the whole run for its band, so a band that saturates early
-    // frees its SM slot instead of idling at the other band's barriers
-    const int tile = kSub > 1 ? item_x / kSub : item_x;
-    const int band = kSub > 1 ? (item_x % kSub) * (16 / kSub) : 0;
+    const int tile = at.tile, band = at.band;
     const int tx = tile % vp.tiles_x, ty = tile / vp.tiles_x;
-    int ox, oy;
-    tile_pixel(ts, threadIdx.x, ox, oy);
-    oy += band;
-    const int px = tx * ts + ox;
-    const int py = ty * ts + oy;
-    const bool inside = px < vp.iw && py < vp.ih;
+    const bool inside = at.inside;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = (nb + 31) >> 5;
     const int wlanes = min(32, nb - warp * 32);
     const unsigned wmask = wlanes == 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
@@ -282,9 +307,22 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
         s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
                                            : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
     }
-    const unsigned *__restrict__ vals = wsv.vals[sorted ? sorted_buffer(wsv.internal) : 0];
+    // the gather's two base pointers live in shared memory and are re-read per
+    // batch (4 registers fewer across the compositing loop)
+    __shared__ __align__(16) const void *s_gather[2];
+    if (threadIdx.x == 0) {
+        s_gather[0] = payload;
+        s_gather[1] = wsv.vals[sorted ? sorted_buffer(wsv.internal) : 0];
+    }
+    auto gather = [&](int64_t e) {
+        const void *pl, *vl;
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(pl), "=l"(vl) : "r"(smem_addr(s_gather)));
+        const unsigned idx = __ldg(static_cast<const unsigned *>(vl) + e);
+        return static_cast<const typename Px<Real>::Payload *>(pl)[idx];
+    };
     const int64_t lo = starts[tile], hi = starts[tile + 1];
-    const Real fx = (Real)px, fy = (Real)py;
+    const Real fx = (Real)at.px, fy = (Real)at.py;
     const Real floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
     const Real half = (Real)-0.5, one = (Real)1;
     // a pixel is finished once T < t_stop (T never grows); pixels outside the
@@ -310,7 +348,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
 
     typename Px<Real>::Payload pre;
     bool have = lo + threadIdx.x < hi;
-    if (have) pre = payload[vals[lo + threadIdx.x]];
+    if (have) pre = gather(lo + threadIdx.x);
     stage(lo, 0, pre, have);
     __syncthreads();
     int buf = 0;
@@ -318,7 +356,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
         // issue the next batch's gather now; it lands while this batch composites
         const int64_t e1 = b0 + nb + threadIdx.x;
         const bool have1 = e1 < hi;
-        if (have1) pre = payload[vals[e1]];
+        if (have1) pre = gather(e1);
         const uint32_t bsp = sp_base + (uint32_t)(buf * nb) * (uint32_t)sizeof(S);
         const uint32_t bmask = mask_base + (uint32_t)(buf * nb) * 4u;
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
@@ -377,8 +415,13 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
         stage(b0 + nb, buf ^ 1, pre, have1);
         if (__syncthreads_count(!(T < t_stop)) == 0) break;
     }
-    if (inside) {
-        const int64_t p = (int64_t)py * vp.iw + px;
+    const Where fin = where();
+    if (fin.inside) {
+        const ViewOut &out = bt.out[fin.view];
+        Real *__restrict__ image = static_cast<Real *>(out.image);
+        Real *__restrict__ final_t = static_cast<Real *>(out.final_t);
+        int32_t *__restrict__ last_contrib = out.last_contrib;
+        const int64_t p = (int64_t)fin.py * bt.vp[fin.view].iw + fin.px;
         if (image) {
             if constexpr (sizeof(Real) == 4) {
                 reinterpret_cast<float4 *>(image)[p] = make_float4(ar, ag, ab, aa);
@@ -387,9 +430,9 @@ k_composite(const __grid_constant__ Batch bt, int sorted, int scheduled) {
                 reinterpret_cast<double2 *>(image)[2 * p + 1] = make_double2(ab, aa);
             }
         }
-        if (uint8_t *q = bt.out[view].rgba8) {
+        if (uint8_t *q = out.rgba8) {
             // composite_over (metrics.py:24) then to_rgba_u8 (_png.py:30), in f64
-            const double *bg = bt.out[view].bg;
+            const double *bg = out.bg;
             const double t = 1.0 - (double)aa;
             const double c[3] = {(double)ar + bg[0] * t, (double)ag + bg[1] * t,
                                  (double)ab + bg[2] * t};
@@ -636,13 +679,17 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         const char *e = getenv("G6R_SCHED");
         return e ? atoi(e) : 1;
     }();
-    bool sched = sched_env && vp.tile_size == 16 && grid.x * kCompositeSub <= 65535;
+    // Batches only: with one view the launch is bound by its heaviest CTA's
+    // latency, and longest-first packs the heavy CTAs onto the same SMs (each
+    // then shares its SM with other heavy ones) -- measured 0.35 -> 0.47 ms per
+    // single-view composite; on batches it saves 7-8 % (tools/probe_composite.py).
+    bool sched = sched_env && b.nviews > 1 && vp.tile_size == 16 &&
+                 grid.x * kCompositeSub <= 65535;
     for (int v = 0; v < b.nviews; ++v) sched = sched && b.ws[v].sched && b.ws[v].internal;
     if (sched) {
         k_sched_order<<<1, 1024, 0, st>>>(b);
         trace_mark("sched_order", st);
     }
-    const int sc = sched ? 1 : 0;
     // > 48 KB dynamic smem for large f64 tiles; the attribute is per device
     static std::atomic<unsigned long long> attrs_done{0};
     if (const unsigned long long bit = device_bit(); !(attrs_done.load() & bit)) {
@@ -653,22 +700,29 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         attrs_done.fetch_or(bit);
     }
     if (vp.precision) {
-        if (vp.tile_size == 16)
+        if (vp.tile_size == 16 && sched)
+            k_composite<double, 256 / kCompositeSub, kCompositeSub, false, true>
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16)
             k_composite<double, 256 / kCompositeSub, kCompositeSub>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
+                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
         else
-            k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt, 0);
+            k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
         bool fast = vp.exp_mode == 1;
         for (int v = 0; v < b.nviews; ++v) fast = fast && !b.out[v].rgba8;   // served bytes stay exact
-        if (vp.tile_size == 16 && fast)
-            k_composite<float, 256 / kCompositeSub, kCompositeSub, true>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
+        const dim3 g2(grid.x * kCompositeSub, grid.y);
+        constexpr int nt = 256 / kCompositeSub;
+        if (vp.tile_size == 16 && fast && sched)
+            k_composite<float, nt, kCompositeSub, true, true><<<g2, nt, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16 && fast)
+            k_composite<float, nt, kCompositeSub, true><<<g2, nt, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16 && sched)
+            k_composite<float, nt, kCompositeSub, false, true><<<g2, nt, 0, st>>>(b, srt);
         else if (vp.tile_size == 16)
-            k_composite<float, 256 / kCompositeSub, kCompositeSub>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt, sc);
+            k_composite<float, nt, kCompositeSub><<<g2, nt, 0, st>>>(b, srt);
         else
-            k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt, 0);
+            k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
     }
     trace_mark("composite", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;

@@ -115,8 +115,15 @@ def render_backward(scene, camera, grad_image, group_mask=None,
     f64 forward is recomputed on the device (it is a small part of the cost)."""
     if config.w_mode not in _W_MODES:
         raise ValueError(f"unknown opacity modulation mode {config.w_mode!r}")
-    g = np.asarray(grad_image, dtype=np.float64)
-    if not g.any():
+    g = np.ascontiguousarray(grad_image, dtype=np.float64)
+    want = (int(camera.height), int(camera.width), 4)
+    if g.shape != want:   # diffrender.py:417-420
+        raise InvalidParameterError(
+            f"grad_image shape {g.shape} does not match the rendered image {want}")
+    if not g.any():   # nothing to propagate; the selection policy still applies (:414)
+        cfg = replace(config, precision="f64")
+        _check_config(cfg)
+        _selection(prepare_scene(scene, cfg.w_mode), group_mask, cfg, RenderStats())
         return GradientBuffer.zeros(len(scene.mu_p))
     return render_backward_device(scene, camera, g, group_mask, config).to_host()
 
@@ -564,6 +571,12 @@ def finetune(scene, views, iters: int = 300, loss_cfg: LossConfig = None,
         raise InvalidParameterError("finetune needs at least one view")
     if iters < 0:
         raise InvalidParameterError(f"iters must be non-negative, got {iters}")
+    if iters == 0:   # the reference returns its input scene object untouched (:571-585)
+        if trace_path is not None:
+            write_trace([], trace_path)
+        if checkpoint_path is not None:
+            save_checkpoint(scene, init_optimizer(scene, 1, base_lr, lr_scale), checkpoint_path)
+        return scene, []
     tr = DeviceTrainer(scene, views, loss_cfg, config, total_steps=max(iters, 1),
                        base_lr=base_lr, lr_scale=lr_scale)
     rng = np.random.default_rng(seed)

@@ -144,7 +144,8 @@ def test_finetune_through_reference_cli_module(splat):
     np.testing.assert_allclose(got_scene.mu_p, want_scene.mu_p, rtol=1e-6, atol=1e-12)
 
 
-REF_SUITES = ["test_raster.py", "test_acceptance.py", "test_service.py", "test_metrics.py"]
+REF_SUITES = ["test_raster.py", "test_acceptance.py", "test_service.py", "test_metrics.py",
+              "test_diffrender.py"]
 
 
 @pytest.mark.parametrize("suite", REF_SUITES)
