@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--batch", "--concurrency", dest="concurrency", type=int, default=16,
                     help="views per kernel launch (1..32; 1 = one view at a time)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-legs", action="store_true",
+                    help="skip the configs[3] (1024x1024) and configs[4] (fine-tune) legs")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="N > 1 transport; gloo lets ranks share one device (tests)")
     ap.add_argument("--exp", choices=("fast", "exact"), default="fast",
                     help="f32 compositor exp: SFU ex2 (image within the 1e-3 / 60 dB parity "
                          "bound) or glibc expf restated (framebuffer bit-identical)")
@@ -70,12 +74,16 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic():
-    """dram bytes per composite launch from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+PROFILE = os.path.join(ROOT, "profiles", "r2_kernels.json")
+
+
+def load_profile():
+    """Per-kernel ncu table of the bench's own views (tools/launch_table.py,
+    committed under profiles/): DRAM bytes per compositor launch and per view
+    of the whole path, measured by the DRAM counters."""
     try:
-        with open(path) as fh:
-            return json.load(fh).get("composite_dram_bytes_per_launch")
+        with open(PROFILE) as fh:
+            return json.load(fh)
     except Exception:
         return None
 
@@ -161,9 +169,31 @@ def reference_scene(scene):
                     spatial_scale=scene.spatial_scale, directional_scale=scene.directional_scale)
 
 
-def time_reference(scene, cams, seconds, max_views):
+def cpu_model():
+    """Host CPU model name (lscpu, else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def time_reference(scene, cams, seconds, max_views, keep=0, extras=False):
     """Reference CPU renderer (oracle/_ref: splatct with its OpenMP kernels) on
-    all host cores: prep once, one warm-up view, then views until `seconds`."""
+    all host cores: prep once, one warm-up view, then views until `seconds`.
+    keep: return the images of the first `keep` timed views (cams[1..keep])
+    for the parity readout; extras: also one view on 1 thread and the sorted
+    runs of cams[1] (render_with_state), both untimed for the headline."""
     ref_dir = os.path.join(ROOT, "oracle", "_ref")
     if not os.path.isdir(os.path.join(ref_dir, "splatct")):
         return None
@@ -177,21 +207,153 @@ def time_reference(scene, cams, seconds, max_views):
     R.prepare_scene(rs, "peak")
     prep_s = time.perf_counter() - t0
     R.render(rs, cams[0], config=cfg)
-    times = []
+    times, images = [], {}
     t_start = time.perf_counter()
     k = 0
     while k < max_views and (k < 2 or time.perf_counter() - t_start < seconds):
         t = time.perf_counter()
-        R.render(rs, cams[(k + 1) % len(cams)], config=cfg)
+        img = R.render(rs, cams[(k + 1) % len(cams)], config=cfg)
         times.append(time.perf_counter() - t)
+        if k < keep:
+            images[(k + 1) % len(cams)] = img
         k += 1
     total = sum(times)
-    return dict(value=len(times) / total, unit=UNIT, cores=cores, kind="reference",
-                sample=f"{len(times)} orbit views of the same 1M scene at {cams[0].width}x"
-                       f"{cams[0].height}, f32, splatct 0.1.0 compiled (Cython/OpenMP, "
-                       f"threads={cores}); prep {prep_s:.2f}s excluded; median "
-                       f"{statistics.median(times):.3f} s/view",
-                prep_s=prep_s)
+    res = dict(value=len(times) / total, unit=UNIT, cores=cores, kind="reference",
+               sample=f"{len(times)} orbit views of the same 1M scene at {cams[0].width}x"
+                      f"{cams[0].height}, f32, splatct 0.1.0 compiled (Cython/OpenMP, "
+                      f"threads={cores}); prep {prep_s:.2f}s excluded; median "
+                      f"{statistics.median(times):.3f} s/view",
+               prep_s=prep_s, images=images, cpu_model=cpu_model())
+    if extras:
+        t = time.perf_counter()
+        R.render(rs, cams[1], config=R.RenderConfig(precision="f32", threads=1))
+        res["single_thread_s_per_view"] = time.perf_counter() - t
+        st = R.render_with_state(rs, cams[1], config=cfg)
+        res["runs"] = (st.entries.entry_splat, st.entries.tile_starts, st.image)
+    return res
+
+
+def parity_readout(scene, cams, ref, images, cap):
+    """GPU vs the reference on the same views (SURVEY appendix A gates 2-3):
+    the headline (fast-exp) images of the views the CPU baseline rendered, the
+    exact mode's bitwise equality, and the benchmarked path's sorted runs of
+    one view against the reference's render_with_state."""
+    import torch
+    from paper_2505_17338_b200 import raster
+    from paper_2505_17338_b200.raster import RenderConfig
+    idx = sorted(ref["images"])
+    want = np.stack([ref["images"][v] for v in idx]).astype(np.float64)
+    got = images[idx].double().cpu().numpy()
+    d = got[..., :3] - want[..., :3]
+    mse = np.maximum((d * d).reshape(len(idx), -1).mean(1), 1e-30)
+    out = {"views": idx, "max_abs": float(np.abs(got - want).max()),
+           "min_psnr_db": float((10.0 * np.log10(1.0 / mse)).min()),
+           "bitwise_equal_pixels": float((got == want).all(-1).mean()),
+           "pixels_over_1e-4": int((np.abs(got - want) > 1e-4).any(-1).sum())}
+    exact = raster.render_views(scene, [cams[v] for v in idx], config=RenderConfig(), capacity=cap)[0]
+    want_f32 = np.stack([ref["images"][v] for v in idx])
+    out["exact_mode_bitwise"] = bool(np.array_equal(exact.cpu().numpy(), want_f32))
+    if "runs" in ref:
+        es_ref, ts_ref, _ = ref["runs"]
+        H, W = cams[1].height, cams[1].width
+        T = ((W + 15) // 16) * ((H + 15) // 16)
+        es = torch.empty((1, cap), dtype=torch.int32, device="cuda")
+        ts = torch.empty((1, T + 1), dtype=torch.int64, device="cuda")
+        _, c = raster.render_views(scene, [cams[1]], config=RenderConfig(exp_mode="fast"),
+                                   capacity=cap, entry_splat=es, tile_starts=ts)
+        e = int(c[0, 1].item())
+        es = es[0, :e].cpu().numpy()
+        n = min(len(es), len(es_ref))
+        out["runs_view"] = 1
+        out["runs_equal"] = bool(len(es) == len(es_ref) and np.array_equal(es, es_ref)
+                                 and np.array_equal(ts[0].cpu().numpy(), ts_ref))
+        out["key_mismatches"] = int((es[:n] != es_ref[:n]).sum()) + abs(len(es) - len(es_ref))
+    return out
+
+
+def leg_1024(scene, lo, hi, args, views=16):
+    """BASELINE configs[3] on one GPU: the same scene at 1024x1024, views
+    0..views-1 of the 800-view orbit (the block rank 0 of a sharded run owns
+    first), timed like the headline (CUDA events around render_views)."""
+    import torch
+    from paper_2505_17338_b200 import _native as nat
+    from paper_2505_17338_b200 import raster
+    from paper_2505_17338_b200.raster import RenderConfig
+    cfg = RenderConfig(exp_mode=args.exp)
+    cams = orbit_from_bbox(lo, hi, 800, 1024)[:views]
+    _, cnt = raster.render_views(scene, cams, config=cfg)
+    torch.cuda.synchronize()
+    cnt = cnt.cpu().numpy()
+    cap = int(cnt[:, nat.CNT_ENTRIES].max() * 1.25) + 65536
+    out = torch.empty((views, 1024, 1024, 4), dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        raster.render_views(scene, cams, config=cfg, capacity=cap, out=out, concurrency=args.concurrency)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, cnt = raster.render_views(scene, cams, config=cfg, capacity=cap, out=out,
+                                 concurrency=args.concurrency)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = nat.Profiler(views)
+    raster.render_views(scene, cams, config=cfg, capacity=cap, out=out, profiler=prof,
+                        concurrency=args.concurrency)
+    stage, nv = prof.read()
+    prof.close()
+    c = cnt.cpu().numpy()
+    return {"workload": "cfg4: same 1M scene, 1024x1024, views 0..%d of the 800-view orbit" % (views - 1),
+            "views": views, "value": views / (ms / 1e3), "unit": UNIT,
+            "ms_per_view": ms / views, "overflowed_views": int(c[:, nat.CNT_OVERFLOW].sum()),
+            "mean_entries": float(c[:, nat.CNT_ENTRIES].mean()),
+            "stage_ms_per_view": {k: v / max(nv, 1) for k, v in stage.items()}}
+
+
+def leg_finetune(scene, lo, hi, iters=20, ref_iteration=True):
+    """BASELINE configs[4]: the fine-tune loop on the 1M scene at 512x512
+    (f64 forward + L1/MS-SSIM loss + backward + Adam per iteration, all on the
+    device, diffrender.DeviceTrainer), 8 orbit views with synthetic targets;
+    ms per iteration over `iters` iterations after 3 warm-up ones.  One
+    iteration of the reference's own loop body (diffrender.py:570-581) on the
+    host cores is timed beside it."""
+    import torch
+    from paper_2505_17338_b200 import diffrender as D
+    from paper_2505_17338_b200 import scenes
+    cams = orbit_from_bbox(lo, hi, 8, 512)
+    views = [(c, scenes.synthetic_target(512, 512, seed=k)) for k, c in enumerate(cams)]
+    tr = D.DeviceTrainer(scene, views, total_steps=300)
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        tr.step(int(rng.integers(len(views))))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rows = [tr.step(int(rng.integers(len(views)))) for _ in range(iters)]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    out = {"workload": "cfg5: fine-tune loop on the same 1M scene, 512x512, 8 orbit views, "
+                       "synthetic targets", "iters": iters, "ms_per_iter": ms,
+           "projected_300_iters_s": 0.3 * ms, "last_loss": rows[-1]["total"]}
+    del tr
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if ref_iteration and os.path.isdir(os.path.join(ref_dir, "splatct")):
+        if ref_dir not in sys.path:
+            sys.path.insert(0, ref_dir)
+        from splatct import diffrender as RD
+        from splatct import raster as R
+        rs = reference_scene(scene)
+        cfg = R.RenderConfig(precision="f64", threads=os.cpu_count() or 1)
+        opt = RD.init_optimizer(rs, total_steps=300)
+        cam, target = views[0]
+        t = time.perf_counter()
+        st = R.render_with_state(rs, cam, None, cfg)
+        _, _, _, grad = RD._loss_parts(st.image, target, RD.LossConfig())
+        buf = RD.render_backward(rs, cam, grad, config=cfg, state=st)
+        RD.adam_step(opt, buf, rs)
+        out["reference_cpu_s_per_iter"] = time.perf_counter() - t
+        out["reference_cores"] = os.cpu_count()
+    return out
 
 
 def run_reference(args):
@@ -232,10 +394,15 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; with fewer devices than ranks (gloo test runs) ranks share
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     host_scene = make_scene(args.gaussians) if rank == 0 else None
     bcast_ms = 0.0
@@ -390,20 +557,35 @@ def run_b200(args):
         H = W = args.size
         T = ((W + 15) // 16) * ((H + 15) // 16)
         peak, peak_kind = load_peaks()
-        comp_ms = stage_ms["composite"] / max(nviews, 1)
-        comp_bytes = float(np.mean(40.0 * E + 16.0 * H * W))
-        comp_gbs = comp_bytes / (comp_ms / 1e3) / 1e9
+        # the dominant kernel per LAUNCH (one launch = one batch of views)
+        nb_prof = math.ceil(V / max(1, min(args.concurrency, 32)))
+        views_per_launch = V / nb_prof
+        comp_launch_ms = stage_ms["composite"] / nb_prof
+        comp_bytes_view = float(np.mean(40.0 * E + 16.0 * H * W))
+        comp_bytes = comp_bytes_view * views_per_launch
+        comp_gbs = comp_bytes / (comp_launch_ms / 1e3) / 1e9
+        traffic = None
+        if prof_tab and prof_tab.get("composite_dram_bytes_per_launch"):
+            # ncu DRAM counters of the same kernel, scaled to this run's launch size
+            traffic = (prof_tab["composite_dram_bytes_per_launch"] / prof_tab["views_per_launch"]
+                       * views_per_launch)
         view_bytes = float(np.mean(180.0 * n + 64.0 * M + 84.0 * E + 8.0 * T + 16.0 * H * W))
-        traffic = load_traffic()
+        prof_tab = load_profile()
         # launches per batch: clear, project, sort histogram, one onesweep per
         # radix pass (upper bound; surplus passes exit at once), composite, and
         # either the 4 tile-partition kernels (splat-level sort, T <= 4096:
         # depth + sentinel = 33 bits -> 4 passes) or ranges (entry sort)
+        # per batch: clear, project, sort histogram, one onesweep per radix
+        # pass (upper bound; surplus passes exit at once), the compositor work
+        # order and the compositor, and either the 4 tile-partition kernels
+        # (splat-level sort, T <= 4096: depth + sentinel = 33 bits -> 4
+        # passes) or ranges (entry sort)
         batches = math.ceil(V / max(1, min(args.concurrency, 32)))
+        sched = 1 if V > 1 else 0
         if T <= 4096:
-            launches = batches * (4 + 4 + (33 + 8) // 9)
+            launches = batches * (4 + sched + 4 + (33 + 8) // 9)
         else:
-            launches = batches * (5 + (32 + max(1, math.ceil(math.log2(T))) + 8) // 9)
+            launches = batches * (5 + sched + (32 + max(1, math.ceil(math.log2(T))) + 8) // 9)
         line = {
             "metric": METRIC, "value": views_per_s, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / V,
@@ -414,7 +596,10 @@ def run_b200(args):
                        "gaussians": n, "width": W, "height": H, "views_per_gpu": V,
                        "parallelism": f"view-parallel x{world}", "projection_dtype": "f64",
                        "composite_dtype": "f32", "composite_exp": args.exp,
-                       "l2": "inputs larger than L2 (352 MB of prepared records re-read per view)"},
+                       "l2": "inputs larger than L2: the 352 MB of prepared records are read "
+                             "once per batch launch (its views share them through L2) and every "
+                             "view's ~110 MB of sort/partition/payload scratch is rewritten; "
+                             "no explicit flush between timed views"},
             "gaussians_per_s": views_per_s * n,
             "stage_ms_per_view": {k: v / max(nviews, 1) for k, v in stage_ms.items()},
             "mean_drawn": float(M.mean()), "mean_entries": float(E.mean()),
@@ -424,6 +609,11 @@ def run_b200(args):
             # whole path (180 N + 64 M + 84 E + 8 T + 16 HW bytes per view)
             # per GPU against the measured HBM copy peak
             "view_roofline_frac": view_bytes * views_per_s / world / 1e9 / peak,
+            # the same with the DRAM counters (ncu, the bench's views, committed
+            # profile): bytes the whole pass actually moved per view
+            "view_dram_frac": (prof_tab["dram_bytes_per_view"] * views_per_s / world / 1e9 / peak
+                               if prof_tab else None),
+            "view_dram_bytes_source": os.path.relpath(PROFILE, ROOT) if prof_tab else None,
             "other_exp_mode": {"exp": other.exp_mode,
                                "value": world * V / (float(t_other.item()) / 1e3),
                                "framebuffer_vs_headline": mode_diff},
@@ -433,11 +623,15 @@ def run_b200(args):
                          "frac": comp_gbs / peak, "traffic": traffic,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": comp_bytes,
-                         "note": "compositor is issue-bound (FP32 per pixel x entry, + FP64 for the exact expf); "
-                                 "bytes = 40 E + 16 HW per view (SURVEY 8d); launch duration "
-                                 "from CUDA events around each batch's compositor launch in a "
-                                 "second, single-stream pass over the same views (the timed pass "
-                                 "overlaps batches on two streams)"},
+                         "views_per_launch": views_per_launch,
+                         "launch_ms": comp_launch_ms,
+                         "note": "compositor is issue-bound (FP32 per pixel x entry; ncu: 82 % "
+                                 "issue-active, profiles/r2_kernels.json); bytes = 40 E + 16 HW "
+                                 "per view (SURVEY 8d) x views per launch; launch duration from "
+                                 "CUDA events around each batch's compositor launch in a second, "
+                                 "single-stream pass over the same views (the timed pass overlaps "
+                                 "batches on two streams); traffic = ncu DRAM read+write bytes "
+                                 "per launch of the same kernel on the same views"},
             "e2e": {"value": world * V / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 136, "d2h_bytes_per_step": H * W * 16 + 128,
                     "api": "paper_2505_17338_b200.raster.render_batch (numpy images out, "
@@ -447,10 +641,22 @@ def run_b200(args):
             **({"frame_gather": frame_gather} if frame_gather is not None else {}),
             "clocks": clk,
         }
+        if world == 1 and not args.no_legs:
+            line["cfg4_1024"] = leg_1024(scene, lo, hi, args)
         if world == 1 and not args.no_cpu_baseline and host_scene is not None:
-            ref = time_reference(host_scene, cams_all, args.cpu_seconds, 40)
-            line["cpu_baseline"] = ({k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
-                                    if ref else None)
+            keep = min(4, V - 1)
+            ref = time_reference(host_scene, cams_all, args.cpu_seconds, 40, keep=keep, extras=True)
+            if ref:
+                cb = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                cb["cpu_model"] = ref["cpu_model"]
+                cb["single_thread_s_per_view"] = ref.get("single_thread_s_per_view")
+                line["cpu_baseline"] = cb
+                line["parity"] = parity_readout(scene, cams, ref, images, cap)
+            else:
+                line["cpu_baseline"] = None
+        if world == 1 and not args.no_legs:
+            line["cfg5_finetune"] = leg_finetune(scene, lo, hi,
+                                                 ref_iteration=not args.no_cpu_baseline)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -329,6 +329,10 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     // image start finished
     Real T = inside ? one : (Real)0, ar = 0, ag = 0, ab = 0, aa = 0;
     int last = 0;
+    // fast exp: within 2.5e-6 (> 2e-6 + the ex2 error) of the alpha floor the
+    // exact expf decides, so every floor decision is the exact mode's
+    const float floor_lo = (float)(1.0 / 255.0) * (1.0f - 2.5e-6f);
+    const float floor_hi = (float)(1.0 / 255.0) * (1.0f + 2.5e-6f);
     __syncthreads();   // s_wbox / s_tab ready
 
     // stage batch k's entry (this thread's) into buffer `buf`
@@ -360,6 +364,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         const uint32_t bsp = sp_base + (uint32_t)(buf * nb) * (uint32_t)sizeof(S);
         const uint32_t bmask = mask_base + (uint32_t)(buf * nb) * 4u;
         const int cnt = (int)((hi - b0) < nb ? (hi - b0) : nb);
+        const int jbase = (int)(b0 - lo) + 1;   // last_contrib of batch entry j = jbase + j
         if (!__all_sync(wmask, T < t_stop)) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
                 unsigned hits = 0;   // splats c0..c0+31 that can touch this warp
@@ -369,10 +374,14 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                         wmask, lane + k < 32 && jl < cnt && ((lds_u32(bmask + 4u * jl) >> warp) & 1u));
                     hits |= b << k;
                 }
-                while (hits) {
-                    const int j = c0 + __ffs(hits) - 1;
-                    hits &= hits - 1;
-                    if (T < t_stop) continue;
+                // ascending order: walk the bit-reversed mask from its top bit
+                unsigned rh = __brev(hits);
+                while (rh) {
+                    unsigned k;   // leading zeros of rh (FLO.SH)
+                    asm("bfind.shiftamt.u32 %0, %1;" : "=r"(k) : "r"(rh));
+                    rh ^= 0x80000000u >> k;
+                    const int j = c0 + (int)k;
+                    if (T < t_stop) continue;   // the pixel is finished
                     S s;
                     lds_splat(bsp + (uint32_t)j * (uint32_t)sizeof(S), s);
                     Real mx, my, ca, cb, cc, al;
@@ -391,13 +400,18 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                         float e;
                         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
                         ai = al * e;
-                        if (fabsf(ai - floor_a) <= 2e-6f * floor_a) ai = al * splat_exp_s(pw, eops);
-                    } else if constexpr (sizeof(Real) == 8) {
-                        ai = al * exp_glibc(pw, s_tab64);   // libm exp, bit for bit
+                        // one compare in the common case (well above the floor)
+                        if (ai < floor_hi) {
+                            if (ai >= floor_lo) ai = al * splat_exp_s(pw, eops);
+                            if (ai < floor_a) continue;
+                        }
                     } else {
-                        ai = al * splat_exp_s(pw, eops);
+                        if constexpr (sizeof(Real) == 8)
+                            ai = al * exp_glibc(pw, s_tab64);   // libm exp, bit for bit
+                        else
+                            ai = al * splat_exp_s(pw, eops);
+                        if (ai < floor_a) continue;
                     }
-                    if (ai < floor_a) continue;
                     Real r, g, b;
                     colours(s, r, g, b);
                     const Real w = ai * T;
@@ -406,7 +420,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                     ab = ab + b * w;
                     aa = aa + w;
                     T = T * (one - ai);
-                    last = (int)(b0 - lo) + j + 1;
+                    last = jbase + j;
                 }
             }
         }

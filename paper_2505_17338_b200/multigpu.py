@@ -82,8 +82,18 @@ def unpack_scene(params: torch.Tensor, labels: torch.Tensor, scales: torch.Tenso
                        **cols)
 
 
+def _staged(t: torch.Tensor, group) -> torch.Tensor:
+    """gloo moves host tensors only for some collectives: stage device tensors
+    through host memory there (NCCL takes device tensors directly)."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu()
+    return t
+
+
 def broadcast_scene(scene, device, src: int = 0, group=None) -> DeviceScene:
-    """Broadcast ``scene`` (given on ``src``, ignored elsewhere) to every rank.
+    """Broadcast ``scene`` (given on rank ``src`` of ``group``, ignored
+    elsewhere) to every rank of ``group``; ``src`` is a rank *within* the
+    group (the default group: the global rank).
 
     Three collectives in total per scene: the row count, the (N,40) float64
     parameters plus the label bytes, and the 4 scales."""
@@ -91,7 +101,7 @@ def broadcast_scene(scene, device, src: int = 0, group=None) -> DeviceScene:
     n = torch.zeros(1, dtype=torch.int64, device=device)
     if rank == src:
         n[0] = len(scene.mu_p)
-    dist.broadcast(n, src, group=group)
+    n = _bcast(n, src, group)
     n = int(n.item())
     if rank == src:
         params, labels, scales = pack_scene(scene, device)
@@ -99,15 +109,24 @@ def broadcast_scene(scene, device, src: int = 0, group=None) -> DeviceScene:
         params = torch.empty((n, N_PARAMS), dtype=torch.float64, device=device)
         labels = torch.empty(n, dtype=torch.uint8, device=device)
         scales = torch.empty(4, dtype=torch.float64, device=device)
-    dist.broadcast(params, src, group=group)
-    dist.broadcast(labels, src, group=group)
-    dist.broadcast(scales, src, group=group)
+    params = _bcast(params, src, group)
+    labels = _bcast(labels, src, group)
+    scales = _bcast(scales, src, group)
     return unpack_scene(params, labels, scales)
+
+
+def _bcast(t: torch.Tensor, src: int, group) -> torch.Tensor:
+    s = _staged(t, group)
+    dist.broadcast(s, group=group, group_src=src)
+    if s is not t:
+        t.copy_(s)
+    return t
 
 
 def gather_frames(frames: torch.Tensor, n_views: int, dst: int = 0, group=None):
     """Collect every rank's block of served frames on ``dst`` (SURVEY.md 8e,
-    "optionally gather uint8 frames to rank 0").
+    "optionally gather uint8 frames to rank 0"); ``dst`` is a rank within
+    ``group``.
 
     ``frames`` holds this rank's ``shard_views`` block, (V_r, H, W, 4) on its
     device (the blocks differ in length by at most one).  Each rank sends one
@@ -123,8 +142,9 @@ def gather_frames(frames: torch.Tensor, n_views: int, dst: int = 0, group=None):
     per = -(-n_views // world)
     buf = torch.zeros((per,) + tuple(frames.shape[1:]), dtype=frames.dtype, device=frames.device)
     buf[:len(mine)] = frames
+    buf = _staged(buf, group)
     out = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
-    dist.gather(buf, out, dst=dst, group=group)
+    dist.gather(buf, out, group=group, group_dst=dst)
     if rank != dst:
         return None
     return torch.cat([out[r][:len(shard_views(n_views, world, r))] for r in range(world)])

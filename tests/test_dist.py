@@ -114,3 +114,38 @@ def test_data_parallel_finetune_host_logic_world2(tmp_path):
     mp.spawn(_dp_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert (tmp_path / f"dp{r}").read_text() == "ok"
+
+
+def _subgroup_worker(rank, world, port, result_dir):
+    """src/dst are ranks *within* the group: with group = global ranks [1, 2],
+    group rank 0 is global rank 1 (the scene source and the gather target)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        group = dist.new_group([1, 2])
+        ok = True
+        if rank in (1, 2):
+            src_scene = scenes.random_scene(np.random.default_rng(5), 64) if rank == 1 else None
+            ds = multigpu.broadcast_scene(src_scene, torch.device("cpu"), src=0, group=group)
+            want = scenes.random_scene(np.random.default_rng(5), 64)
+            ok = np.array_equal(ds.mu_p.numpy(), want.mu_p)
+            gr = dist.get_rank(group)
+            mine = multigpu.shard_views(5, 2, gr)
+            frames = torch.stack([torch.full((2, 3, 4), v, dtype=torch.uint8) for v in mine])
+            got = multigpu.gather_frames(frames, 5, dst=0, group=group)
+            if rank == 1:
+                ok = ok and got is not None and all(bool((got[v] == v).all()) for v in range(5))
+            else:
+                ok = ok and got is None
+        with open(os.path.join(result_dir, f"sg{rank}"), "w") as fh:
+            fh.write("ok" if ok else "bad")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_and_gather_in_a_subgroup_world3(tmp_path):
+    world = 3
+    mp.spawn(_subgroup_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert (tmp_path / f"sg{r}").read_text() == "ok"
