@@ -565,12 +565,12 @@ def run_b200(args):
         comp_bytes = comp_bytes_view * views_per_launch
         comp_gbs = comp_bytes / (comp_launch_ms / 1e3) / 1e9
         traffic = None
+        prof_tab = load_profile()
         if prof_tab and prof_tab.get("composite_dram_bytes_per_launch"):
             # ncu DRAM counters of the same kernel, scaled to this run's launch size
             traffic = (prof_tab["composite_dram_bytes_per_launch"] / prof_tab["views_per_launch"]
                        * views_per_launch)
         view_bytes = float(np.mean(180.0 * n + 64.0 * M + 84.0 * E + 8.0 * T + 16.0 * H * W))
-        prof_tab = load_profile()
         # launches per batch: clear, project, sort histogram, one onesweep per
         # radix pass (upper bound; surplus passes exit at once), composite, and
         # either the 4 tile-partition kernels (splat-level sort, T <= 4096:
