@@ -415,9 +415,18 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                     Real r, g, b;
                     colours(s, r, g, b);
                     const Real w = ai * T;
-                    ar = ar + r * w;
-                    ag = ag + g * w;
-                    ab = ab + b * w;
+                    if constexpr (kFastExp && sizeof(Real) == 4) {
+                        // fast mode: fused accumulation (one rounding per
+                        // channel instead of two; T, and with it every
+                        // termination decision, is computed as in exact mode)
+                        ar = __fmaf_rn(r, w, ar);
+                        ag = __fmaf_rn(g, w, ag);
+                        ab = __fmaf_rn(b, w, ab);
+                    } else {
+                        ar = ar + r * w;
+                        ag = ag + g * w;
+                        ab = ab + b * w;
+                    }
                     aa = aa + w;
                     T = T * (one - ai);
                     last = jbase + j;
