@@ -43,7 +43,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
         sort_counts, rect, chunk_hist, warp_prefix, tile_total, sched, total;
-    int64_t sort_tiles_cap;
+    int64_t sort_tiles_cap, nrows;
 };
 
 // Per-view workspace layout.  [0, clear_end) is zeroed before every view.
@@ -87,6 +87,7 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     L.sched = o;   // compositor work order (this view's slice of the batch's ranking)
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.total = o;
+    L.nrows = n;
     return L;
 }
 
@@ -110,6 +111,7 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.sched = reinterpret_cast<unsigned *>(b + L.sched);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;
+    w.nrows = L.nrows;
     return w;
 }
 

@@ -8,6 +8,26 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+
+// Bounds checks of the checked build (make EXTRA=-DG6R_CHECKED, tools/
+// checked_build.sh): every index the kernels derive from device-computed
+// offsets (entry slots, sorted positions, splat rows, tile runs) is checked
+// against its buffer, and a violation traps the context (the calling test
+// then fails).  compiled out of the normal build.
+#ifdef G6R_CHECKED
+#define G6R_CHECK(c)                                                                       \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("g6r check failed %s:%d: %s\n", __FILE__, __LINE__, #c);                \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define G6R_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
 
 #include "../../include/g6r.h"
 

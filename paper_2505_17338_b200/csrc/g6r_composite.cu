@@ -319,9 +319,11 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
                      : "=l"(pl), "=l"(vl) : "r"(smem_addr(s_gather)));
         const unsigned idx = __ldg(static_cast<const unsigned *>(vl) + e);
+        G6R_CHECK((int64_t)idx < bt.ws[view].nrows);
         return static_cast<const typename Px<Real>::Payload *>(pl)[idx];
     };
     const int64_t lo = starts[tile], hi = starts[tile + 1];
+    G6R_CHECK(0 <= lo && lo <= hi && (wsv.entry_capacity <= 0 || hi <= wsv.entry_capacity));
     const Real fx = (Real)at.px, fy = (Real)at.py;
     const Real floor_a = (Real)(1.0 / 255.0), t_stop = (Real)1e-4;
     const Real half = (Real)-0.5, one = (Real)1;

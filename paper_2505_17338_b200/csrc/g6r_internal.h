@@ -34,6 +34,7 @@ struct Workspace {
     unsigned *sched;                // T: compositor work items, longest run first (k_sched_order)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
+    int64_t nrows;                  // payload rows (scene rows, or external splats)
 };
 
 // Splat-level sort (g6r_tiles.cu): the hot-path projection writes one depth key

@@ -314,6 +314,7 @@ __device__ __forceinline__ void emit_entries(int nk, int ne, long long e_base, c
         const int ty = es.y0[lo] + q;
         const int tx = es.x0[lo] + (loc - q * w);
         const unsigned long long tile = (unsigned long long)ty * (unsigned)tiles_x + (unsigned)tx;
+        G6R_CHECK(tile < (unsigned long long)tiles_x * 65536ull);
         keys[e_base + j] = (tile << 32) | es.db[lo];
         vals[e_base + j] = es.idx[lo];
     }
@@ -527,6 +528,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
     if (kept && emit_ok) {
         const long long m = kOrdered ? m_base + lm : i;
         if (cnt <= kDirectEntries) {
+            G6R_CHECK(e_base + le + cnt <= ws.entry_capacity);
             unsigned long long *keys = ws.keys[0] + e_base + le;
             unsigned *vals = ws.vals[0] + e_base + le;
             int k = 0;
@@ -559,6 +561,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
                 else if ((r + 1) * w <= k) ++r;
                 const unsigned long long t = (unsigned long long)(es.y0[q] + r) * (unsigned)vp.tiles_x +
                                              (unsigned)(es.x0[q] + (k - r * w));
+                G6R_CHECK(e_base + base + k < ws.entry_capacity);
                 ws.keys[0][e_base + base + k] = (t << 32) | es.db[q];
                 ws.vals[0][e_base + base + k] = es.idx[q];
             }

@@ -350,6 +350,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
             const unsigned d = dr[k] >> 16;
             if (d >= (unsigned)kBins) continue;
             const unsigned pos = s_base[d] + s_wh[warp][d] + (dr[k] & 0xffffu);
+            G6R_CHECK((int64_t)pos < c.e);
             kout[pos] = key[k];
             if (!c.packed) vout[pos] = val[k];
         }

@@ -297,7 +297,12 @@ k_chunk_scatter(const __grid_constant__ Batch b, unsigned long long vmask) {
                 cnt16[t] = (unsigned short)(old + (unsigned)__popc(peers));
             }
             old = __shfl_sync(0xffffffffu, old, leader);
-            if (valid) vals[s_tb[t] + old + (unsigned)__popc(peers & lanemask_lt)] = row;
+            if (valid) {
+                const unsigned pos = s_tb[t] + old + (unsigned)__popc(peers & lanemask_lt);
+                G6R_CHECK(t < (unsigned)T && (int64_t)pos < ws.tile_starts[t + 1] &&
+                          (int64_t)pos < ws.entry_capacity);
+                vals[pos] = row;
+            }
         }
     }
 }
@@ -374,8 +379,10 @@ __global__ void __launch_bounds__(kBlock) k_export_runs(const __grid_constant__ 
     const unsigned *cidx = rank_buffer(ws);
     const unsigned *rows = ws.vals[0];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e;
-         k += (int64_t)gridDim.x * blockDim.x)
+         k += (int64_t)gridDim.x * blockDim.x) {
+        G6R_CHECK(cidx[rows[k]] < (unsigned)c.m);
         out[k] = (int32_t)cidx[rows[k]];
+    }
 }
 
 static size_t scatter_smem_bytes(int tiles) {
