@@ -20,9 +20,6 @@
 
 namespace g6r {
 
-#ifndef G6R_BAND_PER
-#define G6R_BAND_PER 2   // entries staged per thread per batch in k_composite_bands
-#endif
 #ifndef G6R_SCHED_MINB
 #define G6R_SCHED_MINB 0   // min CTAs/SM for the scheduled f32 compositor (A/B knob)
 #endif
@@ -474,247 +471,6 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     }
 }
 
-// --- f32 band compositor with asynchronous staging (the hot path) ------------
-// Same pixel arithmetic, order and decisions as k_composite<float, 128, 2>
-// (16x16 tiles, two 16x8 band CTAs of 4 warps, 8x4 pixels per warp), but the
-// run is staged differently: each batch of kB entries (kB = kPer x 128) is
-// copied payload by payload from L2 into shared memory with cp.async (3 x 16
-// bytes per 48-byte payload) while the previous batch composites, and the
-// per-warp culling masks are computed from the landed copies after that
-// batch's compositing.  No payload is held in registers across the hit loop
-// (12 registers fewer than register staging), so a batch can be several
-// entries per thread -- fewer CTA barriers per run -- at the same occupancy.
-// The entry index of the next-but-one batch is loaded a batch ahead.
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <bool kFastExp, bool kSched, int kPer>
-__global__ void __launch_bounds__(128)
-k_composite_bands(const __grid_constant__ Batch bt, int sorted) {
-    constexpr int kNB = 128, kB = kPer * kNB;
-    __shared__ __align__(16) PayloadF32 s_pl[2][kB];
-    __shared__ unsigned s_mask[2][kB];
-    __shared__ unsigned long long s_tab[32];
-    __shared__ float4 s_wbox[4];
-    __shared__ unsigned s_item;
-    __shared__ __align__(16) const void *s_gather[2];
-    if (kSched) {
-        if (threadIdx.x == 0) {
-            const unsigned k = (unsigned)atomicAdd(
-                reinterpret_cast<unsigned long long *>(&bt.ws[0].internal[kTicketComposite]), 1ull);
-            const int T = bt.vp[0].tiles_x * bt.vp[0].tiles_y;
-            const unsigned r = k >> 1;
-            const unsigned it = bt.ws[r / T].sched[r % T];
-            s_item = ((it >> 16) << 16) | ((it & 0xffffu) * 2 + (k & 1));
-        }
-        __syncthreads();
-    }
-    struct Where {
-        int view, tile, band, px, py;
-        bool inside;
-    };
-    // (view, pixel), derived again in the epilogue instead of kept live
-    auto where = [&]() {
-        Where w;
-        int item_x;
-        if (kSched) {
-            unsigned it;
-            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(it) : "r"(smem_addr(&s_item)));
-            w.view = (int)(it >> 16);
-            item_x = (int)(it & 0xffffu);
-        } else {
-            w.view = blockIdx.y;
-            item_x = blockIdx.x;
-        }
-        const ViewParams &v = bt.vp[w.view];
-        w.tile = item_x >> 1;
-        w.band = (item_x & 1) * 8;
-        int ox, oy;
-        tile_pixel(16, threadIdx.x, ox, oy);
-        w.px = (w.tile % v.tiles_x) * 16 + ox;
-        w.py = (w.tile / v.tiles_x) * 16 + oy + w.band;
-        w.inside = w.px < v.iw && w.py < v.ih;
-        return w;
-    };
-    const Where at = where();
-    const ViewParams &vp = bt.vp[at.view];
-    const Workspace &wsv = bt.ws[at.view];
-    for (int k = threadIdx.x; k < 32; k += kNB) s_tab[k] = c_expf_tab[k];
-    const ExpOperands eops = exp_operands(smem_addr(s_tab));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tx = at.tile % vp.tiles_x, ty = at.tile / vp.tiles_x;
-    if (threadIdx.x < 4) {   // pixel-centre box of warp w, clipped to the image
-        const int w = threadIdx.x;
-        const int x0 = (w & 1) * 8 + tx * 16, y0 = (w >> 1) * 4 + at.band + ty * 16;
-        const int x1 = min(x0 + 7, vp.iw - 1), y1 = min(y0 + 3, vp.ih - 1);
-        s_wbox[w] = (x0 <= x1 && y0 <= y1) ? make_float4((float)x0, (float)x1, (float)y0, (float)y1)
-                                           : make_float4(1e30f, -1e30f, 1e30f, -1e30f);
-    }
-    if (threadIdx.x == 0) {
-        s_gather[0] = wsv.payload;
-        s_gather[1] = wsv.vals[sorted ? sorted_buffer(wsv.internal) : 0];
-    }
-    const int64_t lo = wsv.tile_starts[at.tile], hi = wsv.tile_starts[at.tile + 1];
-    G6R_CHECK(0 <= lo && lo <= hi && (wsv.entry_capacity <= 0 || hi <= wsv.entry_capacity));
-    const float fx = (float)at.px, fy = (float)at.py;
-    const float floor_a = (float)(1.0 / 255.0), t_stop = 1e-4f;
-    const float floor_lo = floor_a * (1.0f - 2.5e-6f), floor_hi = floor_a * (1.0f + 2.5e-6f);
-    float T = at.inside ? 1.0f : 0.0f, ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
-    int last = 0;
-    const uint32_t pl_base = smem_addr(&s_pl[0][0]), mask_base = smem_addr(&s_mask[0][0]);
-    __syncthreads();   // s_wbox, s_tab, s_gather
-
-    auto bases = [&](const PayloadF32 *&pl, const unsigned *&vl) {
-        const void *a, *b;
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
-                     : "=l"(a), "=l"(b) : "r"(smem_addr(s_gather)));
-        pl = static_cast<const PayloadF32 *>(a);
-        vl = static_cast<const unsigned *>(b);
-    };
-    // entry indices of a batch (this thread's kPer entries); -1u past the run
-    auto load_idx = [&](int64_t b0, unsigned (&idx)[kPer]) {
-        const PayloadF32 *pl;
-        const unsigned *vl;
-        bases(pl, vl);
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int64_t e = b0 + q * kNB + threadIdx.x;
-            idx[q] = e < hi ? __ldg(vl + e) : 0xffffffffu;
-        }
-    };
-    auto issue = [&](int buf, const unsigned (&idx)[kPer]) {
-        const PayloadF32 *pl;
-        const unsigned *vl;
-        bases(pl, vl);
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            if (idx[q] == 0xffffffffu) continue;
-            G6R_CHECK((int64_t)idx[q] < bt.ws[at.view].nrows);
-            const char *src = reinterpret_cast<const char *>(pl + idx[q]);
-            const uint32_t dst = pl_base + (uint32_t)((buf * kB + q * kNB + threadIdx.x) * sizeof(PayloadF32));
-            cp_async16(dst, src);
-            cp_async16(dst + 16, src + 16);
-            cp_async16(dst + 32, src + 32);
-        }
-        cp_async_commit();
-    };
-    // after the copies of `buf` landed: this thread's entries' warp masks
-    auto finish = [&](int buf, const unsigned (&idx)[kPer]) {
-        cp_async_wait_all();
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            if (idx[q] == 0xffffffffu) continue;
-            const int j = q * kNB + threadIdx.x;
-            const float4 a = s_pl[buf][j].a, c = s_pl[buf][j].c;
-            unsigned m = 0;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const float4 bx = s_wbox[w];
-                if (a.x + c.y >= bx.x && a.x - c.y <= bx.y && a.y + c.z >= bx.z && a.y - c.z <= bx.w)
-                    m |= 1u << w;
-            }
-            s_mask[buf][j] = m;
-        }
-    };
-
-    unsigned cur[kPer], nxt[kPer];
-    load_idx(lo, cur);
-    issue(0, cur);
-    load_idx(lo + kB, nxt);
-    finish(0, cur);
-    __syncthreads();
-    int buf = 0;
-    for (int64_t b0 = lo; b0 < hi; b0 += kB, buf ^= 1) {
-        // the next batch's copies fly while this one composites; the index
-        // load for the one after goes out now too
-        issue(buf ^ 1, nxt);
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) cur[q] = nxt[q];
-        load_idx(b0 + 2 * kB, nxt);
-        const uint32_t bpl = pl_base + (uint32_t)(buf * kB) * (uint32_t)sizeof(PayloadF32);
-        const uint32_t bmask = mask_base + (uint32_t)(buf * kB) * 4u;
-        const int cnt = (int)((hi - b0) < kB ? (hi - b0) : kB);
-        const int jbase = (int)(b0 - lo) + 1;
-        if (!__all_sync(0xffffffffu, T < t_stop)) {
-            for (int c0 = 0; c0 < cnt; c0 += 32) {
-                const int jl = c0 + lane;
-                const unsigned hits = __ballot_sync(
-                    0xffffffffu, jl < cnt && ((lds_u32(bmask + 4u * jl) >> warp) & 1u));
-                unsigned rh = __brev(hits);
-                while (rh) {
-                    unsigned k;
-                    asm("bfind.shiftamt.u32 %0, %1;" : "=r"(k) : "r"(rh));
-                    rh ^= 0x80000000u >> k;
-                    const int j = c0 + (int)k;
-                    if (T < t_stop) continue;
-                    float4 a, b, c;
-                    const uint32_t ad = bpl + (uint32_t)j * (uint32_t)sizeof(PayloadF32);
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(ad));
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];"
-                                 : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "r"(ad));
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+32];"
-                                 : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w) : "r"(ad));
-                    const float dx = fx - a.x;
-                    const float dy = fy - a.y;
-                    const float pw = -0.5f * (a.z * dx * dx + b.x * dy * dy) - a.w * dx * dy;
-                    if (pw > 0.0f || pw < c.w) continue;   // c.w: power floor (>= -4.5)
-                    float ai;
-                    if constexpr (kFastExp) {
-                        float e;
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
-                        ai = b.y * e;
-                        if (ai < floor_hi) {
-                            if (ai >= floor_lo) ai = b.y * splat_exp_s(pw, eops);
-                            if (ai < floor_a) continue;
-                        }
-                    } else {
-                        ai = b.y * splat_exp_s(pw, eops);
-                        if (ai < floor_a) continue;
-                    }
-                    const float w = ai * T;
-                    if constexpr (kFastExp) {
-                        ar = __fmaf_rn(b.z, w, ar);
-                        ag = __fmaf_rn(b.w, w, ag);
-                        ab = __fmaf_rn(c.x, w, ab);
-                    } else {
-                        ar = ar + b.z * w;
-                        ag = ag + b.w * w;
-                        ab = ab + c.x * w;
-                    }
-                    aa = aa + w;
-                    T = T * (1.0f - ai);
-                    last = jbase + j;
-                }
-            }
-        }
-        if (b0 + kB < hi) finish(buf ^ 1, cur);
-        if (__syncthreads_count(!(T < t_stop)) == 0) break;
-    }
-    cp_async_wait_all();   // copies of a batch the loop broke out before reading
-    const Where fin = where();
-    if (fin.inside) {
-        const ViewOut &out = bt.out[fin.view];
-        const int64_t p = (int64_t)fin.py * bt.vp[fin.view].iw + fin.px;
-        if (out.image) reinterpret_cast<float4 *>(out.image)[p] = make_float4(ar, ag, ab, aa);
-        if (uint8_t *q = out.rgba8) {
-            const double *bg = out.bg;
-            const double t = 1.0 - (double)aa;
-            const double cc[3] = {(double)ar + bg[0] * t, (double)ag + bg[1] * t,
-                                  (double)ab + bg[2] * t};
-            unsigned char u[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) u[k] = (unsigned char)rint(fmin(fmax(cc[k], 0.0), 1.0) * 255.0);
-            reinterpret_cast<uchar4 *>(q)[p] = make_uchar4(u[0], u[1], u[2], 255);
-        }
-        if (out.final_t) static_cast<float *>(out.final_t)[p] = T;
-        if (out.last_contrib) out.last_contrib[p] = last;
-    }
-}
-
 // Compositor work order for a batch: every (view, tile) item ranked by its run
 // length, longest first (quarter-octave buckets; order inside a bucket is
 // arbitrary -- no pixel depends on which CTA composites it or when).  One CTA:
@@ -982,20 +738,7 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         for (int v = 0; v < b.nviews; ++v) fast = fast && !b.out[v].rgba8;   // served bytes stay exact
         const dim3 g2(grid.x * kCompositeSub, grid.y);
         constexpr int nt = 256 / kCompositeSub;
-        static const int bands_env = [] {   // G6R_BANDS=0: register-staged kernel (A/B probe)
-            const char *e = getenv("G6R_BANDS");
-            return e ? atoi(e) : 1;
-        }();
-        if (vp.tile_size == 16 && bands_env) {
-            if (fast && sched)
-                k_composite_bands<true, true, G6R_BAND_PER><<<g2, nt, 0, st>>>(b, srt);
-            else if (fast)
-                k_composite_bands<true, false, G6R_BAND_PER><<<g2, nt, 0, st>>>(b, srt);
-            else if (sched)
-                k_composite_bands<false, true, G6R_BAND_PER><<<g2, nt, 0, st>>>(b, srt);
-            else
-                k_composite_bands<false, false, G6R_BAND_PER><<<g2, nt, 0, st>>>(b, srt);
-        } else if (vp.tile_size == 16 && fast && sched)
+        if (vp.tile_size == 16 && fast && sched)
             k_composite<float, nt, kCompositeSub, true, true><<<g2, nt, 0, st>>>(b, srt);
         else if (vp.tile_size == 16 && fast)
             k_composite<float, nt, kCompositeSub, true><<<g2, nt, 0, st>>>(b, srt);
