@@ -105,6 +105,33 @@ __device__ __forceinline__ void tile_pixel(int ts, int t, int &dx, int &dy) {
     }
 }
 
+// Grouped hit lists (16x16 tiles split into 16x8 bands, 4 warps of 8x4):
+// the warp's 32 lanes form kG groups of gw x gh pixels, each walking its own
+// hit list, so a small splat costs one pass of the group(s) it can touch
+// rather than of the whole warp.  Lane l of warp w: group g = l / (32/kG),
+// pixel (bx + group origin + lane-in-group offset).
+template <int kG> struct GroupShape;
+template <> struct GroupShape<1> { static constexpr int w = 8, h = 4; };
+template <> struct GroupShape<2> { static constexpr int w = 4, h = 4; };
+template <> struct GroupShape<4> { static constexpr int w = 4, h = 2; };
+template <> struct GroupShape<8> { static constexpr int w = 2, h = 2; };
+
+template <int kG>
+__device__ __forceinline__ void band_pixel(int t, int &dx, int &dy) {
+    constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h, gpr = 8 / gw;
+    const int w = t >> 5, l = t & 31;
+    const int g = l / (32 / kG), i = l % (32 / kG);
+    dx = (w & 1) * 8 + (g % gpr) * gw + i % gw;
+    dy = (w >> 1) * 4 + (g / gpr) * gh + i / gw;
+}
+// bit of the band's sub-block grid (16/gw columns x 8/gh rows, row-major)
+// holding band pixel (dx, dy)
+template <int kG>
+__device__ __forceinline__ int group_bit(int dx, int dy) {
+    constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h;
+    return (dy / gh) * (16 / gw) + dx / gw;
+}
+
 __device__ __forceinline__ float splat_exp(float x, const unsigned long long *tab) {
     return expf_glibc(x, tab);
 }
@@ -198,10 +225,11 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // warp's pixel block; warps then ballot over the batch and visit only splats
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
-template <typename Real, int kNB, int kSub = 1, bool kFastExp = false, bool kSched = false>
+template <typename Real, int kNB, int kSub = 1, bool kFastExp = false, bool kSched = false, int kG = 1>
 __global__ void __launch_bounds__(kNB > 0 ? kNB : 1024, (kSched && sizeof(Real) == 4) ? G6R_SCHED_MINB : 0)
 k_composite(const __grid_constant__ Batch bt, int sorted) {
     constexpr bool scheduled = kSched && kSub > 1;
+    constexpr bool grouped = kG > 1 && kNB == 128 && kSub == 2;
     using S = typename Px<Real>::S;
     // Work item: with `scheduled` (kSub > 1), CTAs take (view, tile) items in
     // k_sched_order's longest-run-first order through a ticket, both bands of
@@ -249,7 +277,10 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         w.tile = kSub > 1 ? item_x / kSub : item_x;
         w.band = kSub > 1 ? (item_x % kSub) * (16 / kSub) : 0;
         int ox, oy;
-        tile_pixel(ts_, threadIdx.x, ox, oy);
+        if constexpr (grouped)
+            band_pixel<kG>(threadIdx.x, ox, oy);
+        else
+            tile_pixel(ts_, threadIdx.x, ox, oy);
         w.px = (w.tile % v.tiles_x) * ts_ + ox;
         w.py = (w.tile / v.tiles_x) * ts_ + oy + w.band;
         w.inside = w.px < v.iw && w.py < v.ih;
@@ -337,6 +368,9 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     const float floor_hi = (float)(1.0 / 255.0) * (1.0f + 2.5e-6f);
     __syncthreads();   // s_wbox / s_tab ready
 
+    // grouped: the band's pixel origin and last pixel inside the image
+    const int gx0 = tx * ts, gy0 = ty * ts + band;
+    const int gxmax = min(15, vp.iw - 1 - gx0), gymax = min(7, vp.ih - 1 - gy0);
     // stage batch k's entry (this thread's) into buffer `buf`
     auto stage = [&](int64_t b0, int buf, const typename Px<Real>::Payload &pl, bool have) {
         if (!have) return;
@@ -345,12 +379,36 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         sp[buf * nb + threadIdx.x] = s;
         const float mx = (float)Px<Real>::mx(s), my = (float)Px<Real>::my(s);
         unsigned m = 0;
-        for (int w = 0; w < nwarps; ++w) {
-            const float4 bx = s_wbox[w];
-            if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) m |= 1u << w;
+        if constexpr (grouped) {
+            // pixel columns/rows the box can touch: x >= fl(mx - ex) and
+            // x <= fl(mx + ex), the same float tests as the per-warp box
+            constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h, ncol = 16 / gw;
+            const int xl = max(__float2int_ru(mx - ex) - gx0, 0);
+            const int xh = min(__float2int_rd(mx + ex) - gx0, gxmax);
+            const int yl = max(__float2int_ru(my - ey) - gy0, 0);
+            const int yh = min(__float2int_rd(my + ey) - gy0, gymax);
+            if (xl <= xh && yl <= yh) {
+                const unsigned cols = (2u << (xh / gw)) - (1u << (xl / gw));
+#pragma unroll
+                for (int r = 0; r < 8 / gh; ++r)
+                    if (r >= yl / gh && r <= yh / gh) m |= cols << (r * ncol);
+            }
+        } else {
+            for (int w = 0; w < nwarps; ++w) {
+                const float4 bx = s_wbox[w];
+                if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) m |= 1u << w;
+            }
         }
         smask[buf * nb + threadIdx.x] = m;
     };
+    // grouped: this lane's group; group g of the warp owns sub-block bit
+    // wbase + (g / gpr) * ncol + g % gpr
+    int mygroup = 0, wbase = 0;
+    if constexpr (grouped) {
+        constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h, ncol = 16 / gw;
+        mygroup = lane / (32 / kG);
+        wbase = (warp >> 1) * (4 / gh) * ncol + (warp & 1) * (8 / gw);
+    }
 
     typename Px<Real>::Payload pre;
     bool have = lo + threadIdx.x < hi;
@@ -369,16 +427,31 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         const int jbase = (int)(b0 - lo) + 1;   // last_contrib of batch entry j = jbase + j
         if (!__all_sync(wmask, T < t_stop)) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
-                unsigned hits = 0;   // splats c0..c0+31 that can touch this warp
-                for (int k = 0; k < 32; k += wlanes) {
-                    const int jl = c0 + k + lane;
-                    const unsigned b = __ballot_sync(
-                        wmask, lane + k < 32 && jl < cnt && ((lds_u32(bmask + 4u * jl) >> warp) & 1u));
-                    hits |= b << k;
+                unsigned hits = 0;   // splats c0..c0+31 that can touch this warp (group)
+                if constexpr (grouped) {
+                    constexpr int gw = GroupShape<kG>::w, ncol = 16 / gw, gpr = 8 / gw;
+                    const int jl = c0 + lane;
+                    const unsigned mk = jl < cnt ? lds_u32(bmask + 4u * jl) : 0u;
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) {
+                        const int bit = wbase + (g / gpr) * ncol + g % gpr;
+                        const unsigned b = __ballot_sync(0xffffffffu, (mk >> bit) & 1u);
+                        if (g == mygroup) hits = b;
+                    }
+                } else {
+                    for (int k = 0; k < 32; k += wlanes) {
+                        const int jl = c0 + k + lane;
+                        const unsigned b = __ballot_sync(
+                            wmask, lane + k < 32 && jl < cnt && ((lds_u32(bmask + 4u * jl) >> warp) & 1u));
+                        hits |= b << k;
+                    }
                 }
-                // ascending order: walk the bit-reversed mask from its top bit
+                // ascending order: walk the bit-reversed mask from its top bit;
+                // grouped: the warp iterates as often as its busiest group
                 unsigned rh = __brev(hits);
-                while (rh) {
+                int iters = grouped ? __reduce_max_sync(0xffffffffu, (unsigned)__popc(hits)) : 0;
+                while (grouped ? (iters-- > 0) : (rh != 0u)) {
+                    if (grouped && rh == 0u) continue;
                     unsigned k;   // leading zeros of rh (FLO.SH)
                     asm("bfind.shiftamt.u32 %0, %1;" : "=r"(k) : "r"(rh));
                     rh ^= 0x80000000u >> k;
@@ -692,6 +765,18 @@ int launch_pack_payload(int64_t m, int precision, const void *means2d, const voi
 
 constexpr int kCompositeSub = 2;   // CTAs per 16x16 tile
 
+// f32 band compositor (16x16 tiles, two 16x8 band CTAs) with kG lane groups
+template <bool kFast, bool kSched>
+static void launch_f32_band(int groups, dim3 grid, const Batch &b, int srt, cudaStream_t st) {
+    constexpr int nt = 256 / kCompositeSub;
+    switch (groups) {
+    case 2: k_composite<float, nt, kCompositeSub, kFast, kSched, 2><<<grid, nt, 0, st>>>(b, srt); break;
+    case 4: k_composite<float, nt, kCompositeSub, kFast, kSched, 4><<<grid, nt, 0, st>>>(b, srt); break;
+    case 8: k_composite<float, nt, kCompositeSub, kFast, kSched, 8><<<grid, nt, 0, st>>>(b, srt); break;
+    default: k_composite<float, nt, kCompositeSub, kFast, kSched, 1><<<grid, nt, 0, st>>>(b, srt); break;
+    }
+}
+
 int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     if (b.nviews == 0) return G6R_OK;
     const ViewParams &vp = b.vp[0];
@@ -708,6 +793,14 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
     // latency, and longest-first packs the heavy CTAs onto the same SMs (each
     // then shares its SM with other heavy ones) -- measured 0.35 -> 0.47 ms per
     // single-view composite; on batches it saves 7-8 % (tools/probe_composite.py).
+    // lane groups per warp hit list (f32 band kernels): 8 groups of 2x2 pixels.
+    // cfg3 (tools/probe_bench_views.py, 10-view batches): composite 0.121 ms
+    // per view with one list per warp, 0.107 (2 groups), 0.106 (4), 0.103 (8).
+    // G6R_GROUPS=1|2|4|8 overrides (A/B probe).
+    static const int groups = [] {
+        const char *e = getenv("G6R_GROUPS");
+        return e ? atoi(e) : 8;
+    }();
     bool sched = sched_env && b.nviews > 1 && vp.tile_size == 16 &&
                  grid.x * kCompositeSub <= 65535;
     for (int v = 0; v < b.nviews; ++v) sched = sched && b.ws[v].sched && b.ws[v].internal;
@@ -737,15 +830,14 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         bool fast = vp.exp_mode == 1;
         for (int v = 0; v < b.nviews; ++v) fast = fast && !b.out[v].rgba8;   // served bytes stay exact
         const dim3 g2(grid.x * kCompositeSub, grid.y);
-        constexpr int nt = 256 / kCompositeSub;
         if (vp.tile_size == 16 && fast && sched)
-            k_composite<float, nt, kCompositeSub, true, true><<<g2, nt, 0, st>>>(b, srt);
+            launch_f32_band<true, true>(groups, g2, b, srt, st);
         else if (vp.tile_size == 16 && fast)
-            k_composite<float, nt, kCompositeSub, true><<<g2, nt, 0, st>>>(b, srt);
+            launch_f32_band<true, false>(groups, g2, b, srt, st);
         else if (vp.tile_size == 16 && sched)
-            k_composite<float, nt, kCompositeSub, false, true><<<g2, nt, 0, st>>>(b, srt);
+            launch_f32_band<false, true>(groups, g2, b, srt, st);
         else if (vp.tile_size == 16)
-            k_composite<float, nt, kCompositeSub><<<g2, nt, 0, st>>>(b, srt);
+            launch_f32_band<false, false>(groups, g2, b, srt, st);
         else
             k_composite<float, 0><<<grid, threads, 2 * threads * (sizeof(Px<float>::S) + 4), st>>>(b, srt);
     }
