@@ -20,6 +20,9 @@
 
 namespace g6r {
 
+#ifndef G6R_GROUPED_MINB
+#define G6R_GROUPED_MINB 9   // min CTAs/SM for the grouped f32 compositor (<= 56 registers)
+#endif
 #ifndef G6R_SCHED_MINB
 #define G6R_SCHED_MINB 0   // min CTAs/SM for the scheduled f32 compositor (A/B knob)
 #endif
@@ -115,6 +118,23 @@ template <> struct GroupShape<1> { static constexpr int w = 8, h = 4; };
 template <> struct GroupShape<2> { static constexpr int w = 4, h = 4; };
 template <> struct GroupShape<4> { static constexpr int w = 4, h = 2; };
 template <> struct GroupShape<8> { static constexpr int w = 2, h = 2; };
+
+// 32x32 bit-matrix transpose across a warp: in, lane i bit b; out, lane b
+// bit i (five butterfly stages, each swapping the off-diagonal blocks).
+template <int J, unsigned M0>
+__device__ __forceinline__ unsigned transpose_stage(unsigned x, int lane) {
+    const unsigned y = __shfl_xor_sync(0xffffffffu, x, J);
+    const unsigned hi = (x & ~M0) | ((y & ~M0) >> J);   // lanes with bit J set
+    const unsigned lo = (x & M0) | ((y & M0) << J);
+    return (lane & J) ? hi : lo;
+}
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x, int lane) {
+    x = transpose_stage<16, 0x0000ffffu>(x, lane);
+    x = transpose_stage<8, 0x00ff00ffu>(x, lane);
+    x = transpose_stage<4, 0x0f0f0f0fu>(x, lane);
+    x = transpose_stage<2, 0x33333333u>(x, lane);
+    return transpose_stage<1, 0x55555555u>(x, lane);
+}
 
 template <int kG>
 __device__ __forceinline__ void band_pixel(int t, int &dx, int &dy) {
@@ -226,7 +246,9 @@ __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { r
 // that can touch them, in ascending order (the per-pixel order, hence every
 // bit, is unchanged).
 template <typename Real, int kNB, int kSub = 1, bool kFastExp = false, bool kSched = false, int kG = 1>
-__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024, (kSched && sizeof(Real) == 4) ? G6R_SCHED_MINB : 0)
+__global__ void __launch_bounds__(kNB > 0 ? kNB : 1024,
+                                  (kG > 1 && sizeof(Real) == 4) ? G6R_GROUPED_MINB
+                                  : (kSched && sizeof(Real) == 4) ? G6R_SCHED_MINB : 0)
 k_composite(const __grid_constant__ Batch bt, int sorted) {
     constexpr bool scheduled = kSched && kSub > 1;
     constexpr bool grouped = kG > 1 && kNB == 128 && kSub == 2;
@@ -371,15 +393,17 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
     // grouped: the band's pixel origin and last pixel inside the image
     const int gx0 = tx * ts, gy0 = ty * ts + band;
     const int gxmax = min(15, vp.iw - 1 - gx0), gymax = min(7, vp.ih - 1 - gy0);
-    // stage batch k's entry (this thread's) into buffer `buf`
-    auto stage = [&](int64_t b0, int buf, const typename Px<Real>::Payload &pl, bool have) {
-        if (!have) return;
-        float ex, ey;
-        const S s = Px<Real>::unpack(pl, ex, ey);
-        sp[buf * nb + threadIdx.x] = s;
-        const float mx = (float)Px<Real>::mx(s), my = (float)Px<Real>::my(s);
+    // grouped staging: the entry's box as a mask over the band's 32 sub-blocks
+    // (16/gw columns x 8/gh rows), then the warp's 32 masks (one chunk of 32
+    // entries) transposed so that lane b holds sub-block b's hit word for the
+    // chunk: the hit loop reads its group's word with one shared load
+    auto stage_grouped = [&](int buf, const typename Px<Real>::Payload &pl, bool have) {
         unsigned m = 0;
-        if constexpr (grouped) {
+        if (have) {
+            float ex, ey;
+            const S s = Px<Real>::unpack(pl, ex, ey);
+            sp[buf * nb + threadIdx.x] = s;
+            const float mx = (float)Px<Real>::mx(s), my = (float)Px<Real>::my(s);
             // pixel columns/rows the box can touch: x >= fl(mx - ex) and
             // x <= fl(mx + ex), the same float tests as the per-warp box
             constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h, ncol = 16 / gw;
@@ -393,7 +417,22 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                 for (int r = 0; r < 8 / gh; ++r)
                     if (r >= yl / gh && r <= yh / gh) m |= cols << (r * ncol);
             }
-        } else {
+        }
+        smask[buf * nb + threadIdx.x] = warp_transpose32(m, lane);
+    };
+    // stage batch k's entry (this thread's) into buffer `buf`
+    auto stage = [&](int64_t b0, int buf, const typename Px<Real>::Payload &pl, bool have) {
+        if constexpr (grouped) {   // warp-collective (the transpose below)
+            stage_grouped(buf, pl, have);
+            return;
+        }
+        if (!have) return;
+        float ex, ey;
+        const S s = Px<Real>::unpack(pl, ex, ey);
+        sp[buf * nb + threadIdx.x] = s;
+        const float mx = (float)Px<Real>::mx(s), my = (float)Px<Real>::my(s);
+        unsigned m = 0;
+        {
             for (int w = 0; w < nwarps; ++w) {
                 const float4 bx = s_wbox[w];
                 if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) m |= 1u << w;
@@ -401,13 +440,12 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         }
         smask[buf * nb + threadIdx.x] = m;
     };
-    // grouped: this lane's group; group g of the warp owns sub-block bit
-    // wbase + (g / gpr) * ncol + g % gpr
-    int mygroup = 0, wbase = 0;
+    // grouped: this lane's sub-block (its group's hit word in each chunk)
+    int mybit = 0;
     if constexpr (grouped) {
-        constexpr int gw = GroupShape<kG>::w, gh = GroupShape<kG>::h, ncol = 16 / gw;
-        mygroup = lane / (32 / kG);
-        wbase = (warp >> 1) * (4 / gh) * ncol + (warp & 1) * (8 / gw);
+        int ox, oy;
+        band_pixel<kG>(threadIdx.x, ox, oy);
+        mybit = group_bit<kG>(ox, oy);
     }
 
     typename Px<Real>::Payload pre;
@@ -429,15 +467,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
             for (int c0 = 0; c0 < cnt; c0 += 32) {
                 unsigned hits = 0;   // splats c0..c0+31 that can touch this warp (group)
                 if constexpr (grouped) {
-                    constexpr int gw = GroupShape<kG>::w, ncol = 16 / gw, gpr = 8 / gw;
-                    const int jl = c0 + lane;
-                    const unsigned mk = jl < cnt ? lds_u32(bmask + 4u * jl) : 0u;
-#pragma unroll
-                    for (int g = 0; g < kG; ++g) {
-                        const int bit = wbase + (g / gpr) * ncol + g % gpr;
-                        const unsigned b = __ballot_sync(0xffffffffu, (mk >> bit) & 1u);
-                        if (g == mygroup) hits = b;
-                    }
+                    hits = lds_u32(bmask + 4u * (uint32_t)(c0 + mybit));
                 } else {
                     for (int k = 0; k < 32; k += wlanes) {
                         const int jl = c0 + k + lane;

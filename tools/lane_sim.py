@@ -22,7 +22,7 @@ import oracle as O  # noqa: E402
 from paper_2505_17338_b200 import scenes  # noqa: E402
 from cull_stats import cull_q  # noqa: E402
 
-GROUPS = {1: (8, 4), 2: (4, 4), 4: (4, 2), 8: (2, 2)}
+GROUPS = {1: (8, 4), 2: (4, 4), 4: (4, 2), 8: (2, 2), 16: (2, 1), 32: (1, 1)}
 
 
 def main():
