@@ -479,9 +479,58 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                 // ascending order: walk the bit-reversed mask from its top bit;
                 // grouped: the warp iterates as often as its busiest group
                 unsigned rh = __brev(hits);
-                int iters = grouped ? __reduce_max_sync(0xffffffffu, (unsigned)__popc(hits)) : 0;
-                while (grouped ? (iters-- > 0) : (rh != 0u)) {
-                    if (grouped && rh == 0u) continue;
+                if constexpr (grouped) {
+                    // Branch-free visits: every lane runs the whole visit and
+                    // a lane with nothing to add (its group's list exhausted,
+                    // pixel finished, power out of range, below the alpha
+                    // floor) adds exactly nothing (ai = 0: r*0 = 0, ar + 0 = ar,
+                    // T*1 = T) -- the warp executes the union of the paths
+                    // anyway, so the branches only cost divergence bookkeeping.
+                    for (int it = __reduce_max_sync(0xffffffffu, (unsigned)__popc(hits)); it > 0; --it) {
+                        const bool live = rh != 0u;
+                        unsigned k;   // leading zeros of rh (FLO.SH; ~0 when rh == 0)
+                        asm("bfind.shiftamt.u32 %0, %1;" : "=r"(k) : "r"(rh));
+                        k = live ? k : 0u;
+                        rh &= ~(0x80000000u >> k);
+                        const int j = c0 + (int)k;
+                        S s;
+                        lds_splat(bsp + (uint32_t)j * (uint32_t)sizeof(S), s);
+                        Real mx, my, ca, cb, cc, al;
+                        fields(s, mx, my, ca, cb, cc, al);
+                        const Real dx = fx - mx;
+                        const Real dy = fy - my;
+                        const Real pw = half * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
+                        bool ok = live && !(T < t_stop) && !(pw > (Real)0) && !(pw < power_lo(s));
+                        Real ai;
+                        if constexpr (kFastExp) {
+                            float e;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
+                            ai = al * e;
+                            if (ok && ai < floor_hi && ai >= floor_lo) ai = al * splat_exp_s(pw, eops);
+                        } else {
+                            ai = al * splat_exp_s(pw, eops);
+                        }
+                        ok = ok && !(ai < floor_a);
+                        ai = ok ? ai : (Real)0;
+                        Real r, g, b;
+                        colours(s, r, g, b);
+                        const Real w = ai * T;
+                        if constexpr (kFastExp) {
+                            ar = __fmaf_rn(r, w, ar);
+                            ag = __fmaf_rn(g, w, ag);
+                            ab = __fmaf_rn(b, w, ab);
+                        } else {
+                            ar = ar + r * w;
+                            ag = ag + g * w;
+                            ab = ab + b * w;
+                        }
+                        aa = aa + w;
+                        T = T * (one - ai);
+                        last = ok ? jbase + j : last;
+                    }
+                    continue;
+                }
+                while (rh != 0u) {
                     unsigned k;   // leading zeros of rh (FLO.SH)
                     asm("bfind.shiftamt.u32 %0, %1;" : "=r"(k) : "r"(rh));
                     rh ^= 0x80000000u >> k;
