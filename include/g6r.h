@@ -325,6 +325,14 @@ int g6r_any_nonfinite(int64_t count, const double *x, int32_t *flag, g6r_stream_
  * trace.  Synchronises on the last event. */
 int g6r_trace_dump(const char *path);
 
+/* Zero-copy outputs: the device address of page-locked host memory (the
+ * same pointer on unified-addressing systems).  A g6r_frame's image / rgba8
+ * may point into such memory: the compositor epilogue then writes each
+ * finished pixel over PCIe while the rest of the batch still renders, so host
+ * images need no separate device->host copy after the render.  G6R_EINVAL if
+ * `host` is not page-locked memory visible to the current device. */
+int g6r_host_device_pointer(void *host, void **device);
+
 /* Test probe: y[i] = the device expf used by the f32 compositor (glibc
  * algorithm, g6r_common.cuh) for n floats. */
 int g6r_debug_expf(int64_t n, const float *x, float *y, g6r_stream_t stream);

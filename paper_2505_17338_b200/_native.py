@@ -94,6 +94,7 @@ _SIGS = {
     "g6r_debug_expf": (ctypes.c_int, [I64, P, P, P]),
     "g6r_debug_exp": (ctypes.c_int, [I64, P, P, P]),
     "g6r_trace_dump": (ctypes.c_int, [ctypes.c_char_p]),
+    "g6r_host_device_pointer": (ctypes.c_int, [P, P]),
     "g6r_backward_workspace_bytes": (SZ, [I64, I32, I32, I32, I64]),
     "g6r_render_backward": (ctypes.c_int, [P, U32, P, P, P, SZ, I64, P, P, P, P, P, D, I32, P, P, P,
                                            P, P, P, P, P, P]),

@@ -463,6 +463,17 @@ int g6r_profiler_read(g6r_profiler *p, double *stage_ms, int32_t *views) {
     return cuda_check("profiler read");
 }
 
+int g6r_host_device_pointer(void *host, void **device) {
+    if (!host || !device) return fail(G6R_EINVAL, "host/device pointer is NULL");
+    *device = nullptr;
+    if (cudaHostGetDevicePointer(device, host, 0) != cudaSuccess) {
+        cudaGetLastError();   // not page-locked (or not mapped): clear the sticky-free error
+        *device = nullptr;
+        return fail(G6R_EINVAL, "pointer is not page-locked host memory mapped for the device");
+    }
+    return G6R_OK;
+}
+
 int g6r_trace_dump(const char *path) {
     std::lock_guard<std::mutex> lock(g_trace_mu);
     if (g_trace.empty()) return G6R_OK;

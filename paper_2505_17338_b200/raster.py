@@ -525,6 +525,11 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
 DEFAULT_CONCURRENCY = 16  # views per batched launch (g6r_render_views)
 MAX_BATCH = 32            # kMaxBatch in csrc/g6r_internal.h
 PIPELINE_LANES = int(os.environ.get("G6R_LANES", "2"))   # streams batches alternate over (<= 4)
+# render_batch writing the pinned host images directly from the compositor
+# (G6R_ZERO_COPY=1).  Off by default: measured at cfg3 (20 views), the PCIe
+# stores throttle the compositor -- 3590 views/s end to end against 3870 for
+# device images + overlapped copy-engine D2H (tools/probe_e2e.py)
+ZERO_COPY = os.environ.get("G6R_ZERO_COPY", "0") == "1"
 
 
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
@@ -622,17 +627,24 @@ def _render_lanes(dev):
     return lanes
 
 
+def _host_mapped(t) -> bool:
+    """True when pinned host tensor ``t`` is addressable by the device at its
+    own address (unified addressing), so kernels can write it directly."""
+    dptr = ctypes.c_void_p()
+    rc = nat.load().g6r_host_device_pointer(ctypes.c_void_p(t.data_ptr()), ctypes.byref(dptr))
+    return rc == 0 and dptr.value == t.data_ptr()
+
+
 def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
                  batch: int = DEFAULT_CONCURRENCY) -> np.ndarray:
     """Render many views to host memory: (V, H, W, 4) like stacking
     ``render(scene, cam)`` over ``cameras``.
 
-    Views are rendered ``batch`` per launch, consecutive chunks alternating
-    between two render streams (one chunk's projection and sort overlap the
-    other's compositing); each chunk's images are copied device->host into
-    pinned memory on a side stream while later chunks render.  One
-    synchronisation at the end; views that overflowed the entry capacity are
-    re-rendered individually."""
+    Views are rendered ``batch`` per launch on two alternating streams and
+    each chunk's images are copied device->host into pinned memory on a side
+    stream while later chunks render (with G6R_ZERO_COPY=1 the compositor
+    writes the pinned host images itself instead).  One synchronisation at the end; views that overflowed the entry
+    capacity are re-rendered individually."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cams = list(cameras)
@@ -642,17 +654,28 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     H, W = int(cams[0].height), int(cams[0].width)
     dt = torch.float32 if config.precision == "f32" else torch.float64
     dev = prep.device
-    images = torch.empty((V, H, W, 4), dtype=dt, device=dev)
     # pinned output owned by the returned array (torch's caching host allocator
     # recycles the block once the array is released): no extra host copy
     host = torch.empty((V, H, W, 4), dtype=dt, pin_memory=True)
+    chunk = max(1, min(int(batch), MAX_BATCH))
+    if ZERO_COPY and _host_mapped(host):
+        # zero-copy: the compositor epilogue writes every finished pixel
+        # straight into the pinned host array over PCIe while the rest of the
+        # batch renders -- no device image, no copy after the render
+        _, cnt = render_views(scene, cams, group_mask, config, out=host, concurrency=chunk)
+        cnt = cnt.cpu().numpy()   # synchronises: the kernels that wrote `host` are done
+        out = host.numpy()
+        for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
+            fr, _ = _render_checked(prep, bits, cams[v], config, False)
+            out[v] = fr.image.cpu().numpy()
+        return out
+    images = torch.empty((V, H, W, 4), dtype=dt, device=dev)
     main = torch.cuda.current_stream()
     lanes = _render_lanes(dev)
     copy = lanes[2]
     for ln in lanes:
         ln.wait_stream(main)
     counters = []
-    chunk = max(1, min(int(batch), MAX_BATCH))
     for i, sl in enumerate(_balanced_slices(V, chunk)):
         lane = lanes[i & 1]
         with torch.cuda.stream(lane):
