@@ -134,6 +134,13 @@ typedef struct g6r_frame {
      * alpha 255 (metrics.py:21-25 composite_over, _png.py:21-32 to_rgba_u8). */
     uint8_t *rgba8;
     double background[3];
+    /* Optional page-locked host copies of image / rgba8.  g6r_render_views
+     * copies each view on an internal copy stream as soon as the compositor
+     * has finished that view (a device flag gates the copy), so the transfer
+     * overlaps the rest of the call's rendering; the call stays ordered on its
+     * stream (the copies are joined back before it returns). */
+    void *host_image;
+    uint8_t *host_rgba8;
 } g6r_frame;
 
 const char *g6r_version(void);

@@ -75,7 +75,8 @@ class SplatOut(ctypes.Structure):
 
 class Frame(ctypes.Structure):
     _fields_ = [("image", P), ("final_t", P), ("last_contrib", P), ("counters", P),
-                ("entry_splat", P), ("tile_starts", P), ("rgba8", P), ("background", D * 3)]
+                ("entry_splat", P), ("tile_starts", P), ("rgba8", P), ("background", D * 3),
+                ("host_image", P), ("host_rgba8", P)]
 
 
 _SIGS = {

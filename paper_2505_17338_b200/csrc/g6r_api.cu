@@ -5,6 +5,7 @@
 // synchronises (except g6r_profiler_read, which waits on its own events).
 // Views are rendered in batches: every stage kernel takes up to kMaxBatch views
 // per launch (grid = work x views).
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -42,7 +43,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_counts, rect, chunk_hist, warp_prefix, tile_total, sched, total;
+        sort_counts, rect, chunk_hist, warp_prefix, tile_total, sched, done, total;
     int64_t sort_tiles_cap, nrows;
 };
 
@@ -86,6 +87,8 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
     L.sched = o;   // compositor work order (this view's slice of the batch's ranking)
     o = align_up(o + (size_t)tiles * sizeof(unsigned));
+    L.done = o;    // view-complete flag (reset once per call, not per view)
+    o = align_up(o + sizeof(unsigned));
     L.total = o;
     L.nrows = n;
     return L;
@@ -109,6 +112,7 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.warp_prefix = reinterpret_cast<unsigned *>(b + L.warp_prefix);
     w.tile_total = reinterpret_cast<unsigned *>(b + L.tile_total);
     w.sched = reinterpret_cast<unsigned *>(b + L.sched);
+    w.done_flag = reinterpret_cast<unsigned *>(b + L.done);
     w.entry_capacity = cap;
     w.sort_tiles_cap = L.sort_tiles_cap;
     w.nrows = L.nrows;
@@ -224,6 +228,122 @@ struct g6r_profiler {
 
 namespace g6r {
 
+// --- host copies gated by view completion (g6r_frame.host_image / host_rgba8)
+// cuStreamWaitValue32 (driver entry point, no libcuda link): the copy stream
+// waits until the compositor's last CTA of a view has stored the batch's
+// value into the view's flag, then copies that view while the rest renders.
+typedef int (*WaitValue32Fn)(cudaStream_t, unsigned long long, unsigned, unsigned);
+constexpr unsigned kWaitGeq = 0x0;   // CU_STREAM_WAIT_VALUE_GEQ
+
+static WaitValue32Fn wait_value_fn() {
+    static WaitValue32Fn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return reinterpret_cast<WaitValue32Fn>(p);
+    }();
+    return fn;
+}
+
+static cudaStream_t g_copy[64];
+static std::mutex g_copy_mu;
+static std::vector<cudaEvent_t> g_copy_ev;   // G6R_DEBUG_COPY: one event per finished view copy
+static cudaStream_t copy_stream() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(g_copy_mu);
+    if (!g_copy[dev] && cudaStreamCreateWithFlags(&g_copy[dev], cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    return g_copy[dev];
+}
+
+static bool wants_host_copy(const g6r_frame *frames, int count) {
+    for (int v = 0; v < count; ++v)
+        if (frames[v].host_image || frames[v].host_rgba8) return true;
+    return false;
+}
+
+// zero the done flags of every view slot the call's workspace holds
+__global__ void k_reset_done(char *base, size_t half_bytes, size_t view_bytes, size_t off, int lanes, int nb) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= lanes * nb) return;
+    *reinterpret_cast<unsigned *>(base + (size_t)(k / nb) * half_bytes + (size_t)(k % nb) * view_bytes + off) = 0u;
+}
+
+struct CopyCtx {
+    cudaStream_t cs = nullptr;   // null: no host copies in this call
+    unsigned value = 0;          // batch ordinal + 1 (monotonic per flag slot in a call)
+};
+
+// Start of a call with host copies: reset the flags on `st`, order the copy
+// stream after that.
+static int copy_begin(CopyCtx &cc, char *ws, size_t half_bytes, size_t view_bytes, size_t off, int lanes,
+                      int nb, cudaStream_t st) {
+    cc.cs = copy_stream();
+    if (!cc.cs) return G6R_ECUDA;
+    k_reset_done<<<(unsigned)ceil_div((int64_t)lanes * nb, 128), 128, 0, st>>>(ws, half_bytes, view_bytes, off,
+                                                                               lanes, nb);
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return G6R_ECUDA;
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(cc.cs, ev, 0);
+    cudaEventDestroy(ev);
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
+static void copy_end(const CopyCtx &cc, cudaStream_t st) {
+    if (!cc.cs) return;
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(ev, cc.cs);
+    cudaStreamWaitEvent(st, ev, 0);
+    cudaEventDestroy(ev);
+}
+
+// After a batch's compositor launch on `st`: each view's copies on the copy
+// stream, gated by its flag (or, without stream memory operations, by an event
+// after the batch).
+static int enqueue_host_copies(const Batch &b, const g6r_frame *frames, const CopyCtx &cc, cudaStream_t st) {
+    const WaitValue32Fn wait = wait_value_fn();
+    bool evented = false;
+    for (int v = 0; v < b.nviews; ++v) {
+        const g6r_frame &f = frames[v];
+        if (!f.host_image && !f.host_rgba8) continue;
+        bool gated = false;
+        if (wait && b.out[v].done_flag)
+            gated = wait(cc.cs, (unsigned long long)(uintptr_t)b.out[v].done_flag, b.out[v].done_value, kWaitGeq) == 0;
+        if (!gated && !evented) {
+            cudaEvent_t ev;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return G6R_ECUDA;
+            cudaEventRecord(ev, st);
+            cudaStreamWaitEvent(cc.cs, ev, 0);
+            cudaEventDestroy(ev);
+            evented = true;
+        }
+        static const bool dbg = getenv("G6R_DEBUG_COPY") != nullptr;
+        if (dbg) fprintf(stderr, "g6r copy view %d: wait fn %p gated %d value %u\n", v, (void *)wait, (int)gated,
+                         b.out[v].done_value);
+        const size_t px = (size_t)b.vp[v].iw * b.vp[v].ih;
+        if (f.host_image && f.image)
+            cudaMemcpyAsync(f.host_image, f.image, px * 4 * (b.vp[v].precision ? 8 : 4), cudaMemcpyDeviceToHost,
+                            cc.cs);
+        if (f.host_rgba8 && f.rgba8) cudaMemcpyAsync(f.host_rgba8, f.rgba8, px * 4, cudaMemcpyDeviceToHost, cc.cs);
+        if (dbg) {   // copy-done events, reported by g6r_trace_dump's debug twin below
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) == cudaSuccess) {
+                cudaEventRecord(ev, cc.cs);
+                std::lock_guard<std::mutex> lock(g_copy_mu);
+                g_copy_ev.push_back(ev);
+            }
+        }
+    }
+    return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+}
+
 static void prof_mark(g6r_profiler *p, int k, cudaStream_t st) {
     if (p && p->used < p->max_batches) cudaEventRecord(p->ev[p->used * (G6R_NSTAGES + 1) + k], st);
 }
@@ -232,7 +352,7 @@ static void prof_mark(g6r_profiler *p, int k, cudaStream_t st) {
 static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera *cams, int nviews,
                         const g6r_config *cfg, void *ws_base, size_t ws_bytes, int64_t cap,
                         const g6r_frame *frames, const g6r_splat_out *splats, cudaStream_t st,
-                        g6r_profiler *prof) {
+                        g6r_profiler *prof, const CopyCtx *cc = nullptr) {
     if (!scene || scene->n < 0) return fail(G6R_EINVAL, "scene is NULL or has negative size");
     if (scene->n > 0 && (!scene->records || !scene->flags)) return fail(G6R_EINVAL, "scene arrays are NULL");
     if (nviews < 1 || nviews > kMaxBatch) return fail(G6R_EINVAL, "batch of %d views", nviews);
@@ -257,7 +377,13 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
                            frames[v].counters, frames[v].entry_splat, frames[v].tile_starts,
                            frames[v].rgba8,
                            {frames[v].background[0], frames[v].background[1],
-                            frames[v].background[2]}};
+                            frames[v].background[2]},
+                           nullptr, 0u};
+        if (cc && cc->cs && (frames[v].host_image || frames[v].host_rgba8)) {
+            b.out[v].done_flag = b.ws[v].done_flag;
+            b.out[v].done_value = cc->value;
+            b.signal = 1;
+        }
     }
     if (launch_clear(b, L.clear_end, st)) return cuda_check("clear");
     prof_mark(prof, 0, st);
@@ -277,6 +403,8 @@ static int render_batch(const g6r_scene *scene, uint32_t mask, const g6r_camera 
     }
     if (launch_composite(b, true, st)) return cuda_check("composite");
     prof_mark(prof, 4, st);
+    if (cc && cc->cs)
+        if (enqueue_host_copies(b, frames, *cc, st)) return cuda_check("host copies");
     if (prof && prof->used < prof->max_batches) {
         prof->nv[prof->used++] = nviews;
         prof->views += nviews;
@@ -334,8 +462,25 @@ int g6r_render(const g6r_scene *scene, uint32_t group_mask, const g6r_camera *ca
                g6r_stream_t stream) {
     if (!frame) return fail(G6R_EINVAL, "frame is NULL");
     if (int rc = check_config(cfg)) return rc;
-    return render_batch(scene, group_mask, cam, 1, cfg, workspace, workspace_bytes, entry_capacity,
-                        frame, splats, (cudaStream_t)stream, nullptr);
+    const cudaStream_t st = (cudaStream_t)stream;
+    if (!wants_host_copy(frame, 1))
+        return render_batch(scene, group_mask, cam, 1, cfg, workspace, workspace_bytes, entry_capacity,
+                            frame, splats, st, nullptr);
+    if (!scene || !cam || cam->width < 1 || cam->height < 1 || cfg->tile_size < 1)
+        return render_batch(scene, group_mask, cam, 1, cfg, workspace, workspace_bytes, entry_capacity,
+                            frame, splats, st, nullptr);   // reports the argument error
+    const int64_t tx = (cam->width + cfg->tile_size - 1) / cfg->tile_size;
+    const int64_t ty = (cam->height + cfg->tile_size - 1) / cfg->tile_size;
+    const Layout L = layout(scene->n, tx * ty, entry_capacity, cfg->precision);
+    if (int rc = check_ws(L.total, workspace, workspace_bytes)) return rc;
+    CopyCtx cc;
+    cc.value = 1;
+    if (copy_begin(cc, static_cast<char *>(workspace), L.total, L.total, L.done, 1, 1, st))
+        return cuda_check("copy stream");
+    const int rc = render_batch(scene, group_mask, cam, 1, cfg, workspace, workspace_bytes, entry_capacity,
+                                frame, splats, st, nullptr, &cc);
+    copy_end(cc, st);
+    return rc;
 }
 
 // Two internal streams per device for pipelining consecutive batches: a
@@ -383,14 +528,26 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
     // lanes = how many batch slices the workspace holds (2..kMaxLanes)
     const int lanes = per_batch ? (int)std::min<size_t>(kMaxLanes, workspace_bytes / per_batch) : 1;
     const bool piped = !prof && count > nb && lanes >= 2;
+    // host copies: flags reset for every slot the call uses, copy stream ordered after
+    CopyCtx cc;
+    if (per_batch && wants_host_copy(frames, count)) {
+        const int64_t tx = (cams[0].width + cfg->tile_size - 1) / cfg->tile_size;
+        const int64_t ty = (cams[0].height + cfg->tile_size - 1) / cfg->tile_size;
+        const Layout L = layout(scene->n, tx * ty, entry_capacity, cfg->precision);
+        if (check_ws(per_batch * (piped ? lanes : 1), workspace, workspace_bytes) == G6R_OK &&
+            copy_begin(cc, static_cast<char *>(workspace), per_batch, L.total, L.done, piped ? lanes : 1, nb, st))
+            return cuda_check("copy stream");
+    }
     if (!piped) {
-        for (int32_t k = 0; k < count; k += nb) {
+        int rc = G6R_OK;
+        for (int32_t k = 0, i = 0; k < count && !rc; k += nb, ++i) {
             const int nv = count - k < nb ? count - k : nb;
-            const int rc = render_batch(scene, group_mask, &cams[k], nv, cfg, workspace,
-                                        workspace_bytes, entry_capacity, &frames[k], nullptr, st, prof);
-            if (rc) return rc;
+            cc.value = (unsigned)i + 1;
+            rc = render_batch(scene, group_mask, &cams[k], nv, cfg, workspace, workspace_bytes,
+                              entry_capacity, &frames[k], nullptr, st, prof, &cc);
         }
-        return G6R_OK;
+        copy_end(cc, st);
+        return rc;
     }
     cudaStream_t lane[kMaxLanes];
     if (lane_streams(lane)) return cuda_check("lane streams");
@@ -402,8 +559,9 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
     for (int32_t k = 0, i = 0; k < count && !rc; k += nb, ++i) {
         const int nv = count - k < nb ? count - k : nb;
         char *half = static_cast<char *>(workspace) + (size_t)(i % lanes) * per_batch;
+        cc.value = (unsigned)i + 1;
         rc = render_batch(scene, group_mask, &cams[k], nv, cfg, half, per_batch, entry_capacity,
-                          &frames[k], nullptr, lane[i % lanes], nullptr);
+                          &frames[k], nullptr, lane[i % lanes], nullptr, &cc);
     }
     for (int l = 0; l < lanes; ++l) {   // join (also on error, so the caller's stream stays ordered)
         cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
@@ -412,6 +570,7 @@ int g6r_render_views(const g6r_scene *scene, uint32_t group_mask, const g6r_came
         cudaEventDestroy(join[l]);
     }
     cudaEventDestroy(fork);
+    copy_end(cc, st);
     return rc;
 }
 
@@ -471,6 +630,21 @@ int g6r_host_device_pointer(void *host, void **device) {
         *device = nullptr;
         return fail(G6R_EINVAL, "pointer is not page-locked host memory mapped for the device");
     }
+    return G6R_OK;
+}
+
+// G6R_DEBUG_COPY probe: ms from `start` (an event the caller recorded) to
+// each recorded view copy's completion, printed to stderr, then cleared.
+extern "C" int g6r_debug_copy_times(void *start) {
+    std::lock_guard<std::mutex> lock(g_copy_mu);
+    for (size_t i = 0; i < g_copy_ev.size(); ++i) {
+        float ms = -1.f;
+        cudaEventSynchronize(g_copy_ev[i]);
+        if (start) cudaEventElapsedTime(&ms, (cudaEvent_t)start, g_copy_ev[i]);
+        fprintf(stderr, "g6r copy %zu done at %.3f ms\n", i, ms);
+        cudaEventDestroy(g_copy_ev[i]);
+    }
+    g_copy_ev.clear();
     return G6R_OK;
 }
 

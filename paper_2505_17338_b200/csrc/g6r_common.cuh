@@ -52,6 +52,7 @@ enum {
     kValsBuffer = 9,       // which vals buffer holds the sorted entry values
     kSortPasses = 12,      // radix passes actually needed (decided on the device)
     kTicketComposite = 13, // compositor work-item ticket (slot of the batch's first view)
+    kDoneCount = 14,       // compositor CTAs finished for the view (completion flag, host copies)
     kNumInternal = 16
 };
 

@@ -234,6 +234,26 @@ __device__ __forceinline__ float splat_exp_s(float x, const ExpOperands &e) {
 }
 __device__ __forceinline__ double splat_exp_s(double x, const ExpOperands &) { return exp(x); }
 
+// View completion (g6r_frame.host_image / host_rgba8): every CTA of a view,
+// after its pixels are stored, bumps the view's CTA counter (gpu-scope fence
+// first); the last one publishes done_value to the view's flag with a
+// system-scope release, which gates the host copy enqueued on the copy stream
+// (cuStreamWaitValue32, g6r_api.cu).
+__device__ __forceinline__ void signal_view_done(const Batch &bt, int view, int sub) {
+    __syncthreads();
+    const ViewOut &o = bt.out[view];
+    if (threadIdx.x != 0 || !o.done_flag) return;
+    __threadfence();
+    const unsigned long long total =
+        (unsigned long long)bt.vp[view].tiles_x * bt.vp[view].tiles_y * (unsigned long long)sub;
+    const unsigned long long prev =
+        atomicAdd(reinterpret_cast<unsigned long long *>(&bt.ws[view].internal[kDoneCount]), 1ull);
+    if (prev + 1 == total) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(o.done_flag), "r"(o.done_value) : "memory");
+    }
+}
+
 // One CTA per tile, one thread per pixel.  kNB > 0: compile-time block size
 // (16x16 tiles, static shared memory); kNB == 0: any tile size up to 32x32.
 //
@@ -621,6 +641,7 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         if (final_t) final_t[p] = T;
         if (last_contrib) last_contrib[p] = last;
     }
+    if (bt.signal) signal_view_done(bt, fin.view, kSub);
 }
 
 // Compositor work order for a batch: every (view, tile) item ranked by its run
@@ -637,33 +658,65 @@ __device__ __forceinline__ int sched_bucket(int64_t len) {
     return max(0, kSchedBuckets - 2 - q);     // longer -> earlier
 }
 
+// With completion signalling (host copies) the order is view by view (longer
+// runs first inside a view), so views finish one after another and their
+// copies start while later views composite; a run of k times the batch's mean
+// length is moved k - 1 views earlier (at most 8), so a view's long runs are
+// done by the time its short ones are.
+constexpr int kViewBuckets = 16;   // one per octave of run length
+constexpr int kAllBuckets = kSchedBuckets + kMaxBatch * kViewBuckets;
+__device__ __forceinline__ int sched_bucket_prog(int64_t len, int view, int64_t mean) {
+    const int q = len > 0 ? min(kViewBuckets - 1, (int)__log2f((float)len + 1.0f)) : 0;
+    const int64_t k = len / (mean > 0 ? mean : 1) - 1;
+    const int shift = k < 0 ? 0 : (k > 8 ? 8 : (int)k);
+    return kSchedBuckets + max(0, view - shift) * kViewBuckets + (kViewBuckets - 1 - q);
+}
+
 __global__ void __launch_bounds__(1024) k_sched_order(const __grid_constant__ Batch bt) {
-    __shared__ unsigned s_cnt[kSchedBuckets];
+    __shared__ unsigned s_cnt[kAllBuckets];
+    __shared__ unsigned long long s_sum;
     const int T = bt.vp[0].tiles_x * bt.vp[0].tiles_y;
     const int total = T * bt.nviews;
-    for (int k = threadIdx.x; k < kSchedBuckets; k += blockDim.x) s_cnt[k] = 0;
-    if (threadIdx.x == 0) bt.ws[0].internal[kTicketComposite] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-        const int64_t *st = bt.ws[i / T].tile_starts;
-        const int t = i % T;
-        atomicAdd(&s_cnt[sched_bucket(st[t + 1] - st[t])], 1u);
+    const bool prog = bt.signal != 0;
+    const int nbk = prog ? kAllBuckets : kSchedBuckets;
+    for (int k = threadIdx.x; k < nbk; k += blockDim.x) s_cnt[k] = 0;
+    if (threadIdx.x == 0) {
+        bt.ws[0].internal[kTicketComposite] = 0;
+        s_sum = 0;
     }
+    __syncthreads();
+    int64_t heavy = 0;
+    if (prog) {
+        unsigned long long sum = 0;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) {
+            const int64_t *st = bt.ws[i / T].tile_starts;
+            sum += (unsigned long long)(st[i % T + 1] - st[i % T]);
+        }
+        atomicAdd(&s_sum, sum);
+        __syncthreads();
+        heavy = (int64_t)(s_sum / (unsigned long long)max(total, 1));   // mean run length
+    }
+    auto bucket = [&](int i) {
+        const int v = i / T, t = i % T;
+        const int64_t *st = bt.ws[v].tile_starts;
+        const int64_t len = st[t + 1] - st[t];
+        return prog ? sched_bucket_prog(len, v, heavy) : sched_bucket(len);
+    };
+    for (int i = threadIdx.x; i < total; i += blockDim.x) atomicAdd(&s_cnt[bucket(i)], 1u);
     __syncthreads();
     if (threadIdx.x < 32) {   // exclusive scan of the buckets, one warp
         unsigned carry = 0;
-        for (int b0 = 0; b0 < kSchedBuckets; b0 += 32) {
-            const unsigned x = s_cnt[b0 + threadIdx.x];
+        for (int b0 = 0; b0 < nbk; b0 += 32) {
+            const unsigned x = b0 + threadIdx.x < nbk ? s_cnt[b0 + threadIdx.x] : 0u;
             const unsigned inc = warp_inclusive_scan(x);
-            s_cnt[b0 + threadIdx.x] = carry + inc - x;
+            if (b0 + threadIdx.x < nbk) s_cnt[b0 + threadIdx.x] = carry + inc - x;
             carry += __shfl_sync(0xffffffffu, inc, 31);
         }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
         const int v = i / T, t = i % T;
-        const int64_t *st = bt.ws[v].tile_starts;
-        const unsigned r = atomicAdd(&s_cnt[sched_bucket(st[t + 1] - st[t])], 1u);
+        const unsigned r = atomicAdd(&s_cnt[bucket(i)], 1u);
         bt.ws[r / T].sched[r % T] = ((unsigned)v << 16) | (unsigned)t;
     }
 }

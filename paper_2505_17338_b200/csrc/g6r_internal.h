@@ -32,6 +32,7 @@ struct Workspace {
     unsigned *warp_prefix;          // splat-sort path: per chunk, per scatter warp, packed u16 tile offsets
     unsigned *tile_total;           // splat-sort path: T entry counts
     unsigned *sched;                // T: compositor work items, longest run first (k_sched_order)
+    unsigned *done_flag;            // view-complete flag (not cleared per view; reset per call)
     int64_t entry_capacity;
     int64_t sort_tiles_cap;
     int64_t nrows;                  // payload rows (scene rows, or external splats)
@@ -67,11 +68,14 @@ struct ViewOut {
     int64_t *tile_starts;    // optional copy of the tile ranges
     uint8_t *rgba8;          // optional served frame (composite over bg, quantised)
     double bg[3];
+    unsigned *done_flag;     // when set: the compositor's last CTA of the view stores done_value
+    unsigned done_value;
 };
 
 // One launch's views.  All views share tile size, precision and image size.
 struct Batch {
     int nviews;
+    int signal;   // some view has done_flag: completion signalling + view-major compositor order
     ViewParams vp[kMaxBatch];
     Workspace ws[kMaxBatch];
     ViewOut out[kMaxBatch];

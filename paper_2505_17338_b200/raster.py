@@ -535,7 +535,8 @@ ZERO_COPY = os.environ.get("G6R_ZERO_COPY", "0") == "1"
 def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT_CONFIG,
                  capacity: int | None = None, out=None, profiler=None,
                  concurrency: int = DEFAULT_CONCURRENCY, rgba8=None, background=(0.0, 0.0, 0.0),
-                 image: bool = True, pipeline: bool = True, entry_splat=None, tile_starts=None):
+                 image: bool = True, pipeline: bool = True, entry_splat=None, tile_starts=None,
+                 host_out=None, host_rgba8=None):
     """Render ``cameras`` (same size) with up to ``concurrency`` views in flight.
 
     Returns ``(images, counters)``: ``images`` (V,H,W,4) on the device,
@@ -549,7 +550,11 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     device tensors, when given, receive every view's sorted tile runs exactly
     as ``TileEntries`` holds them (indices into the view's compacted
     SplatBatch, raster.py:201-208); entries past ``counters[v, 1]`` are
-    undefined."""
+    undefined.
+    ``host_out`` / ``host_rgba8`` (pinned CPU tensors shaped like the image /
+    rgba8 outputs) receive each view's copy as soon as the view is complete,
+    overlapped with the rest of the call (g6r_frame.host_image / host_rgba8);
+    they are complete once the current stream reaches the end of the call."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cfg = _check_config(config)
@@ -579,6 +584,12 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     if tile_starts is not None and (tile_starts.dtype != torch.int64 or not tile_starts.is_contiguous()
                                     or tuple(tile_starts.shape) != (V, T + 1)):
         raise InvalidParameterError(f"tile_starts must be a contiguous ({V}, {T + 1}) int64 tensor")
+    for name, t, want in (("host_out", host_out, images), ("host_rgba8", host_rgba8, rgba8)):
+        if t is None:
+            continue
+        if want is None or tuple(t.shape) != tuple(want.shape) or t.dtype != want.dtype \
+                or not t.is_contiguous() or not t.is_pinned():
+            raise InvalidParameterError(f"{name} must be a pinned contiguous CPU tensor shaped like the output")
     slots = max(1, min(int(concurrency), MAX_BATCH, V))
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
@@ -591,7 +602,9 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
                                          counters[v].data_ptr(),
                                          entry_splat[v].data_ptr() if entry_splat is not None else 0,
                                          tile_starts[v].data_ptr() if tile_starts is not None else 0,
-                                         rgba8[v].data_ptr() if rgba8 is not None else 0, bg)
+                                         rgba8[v].data_ptr() if rgba8 is not None else 0, bg,
+                                         host_out[v].data_ptr() if host_out is not None else 0,
+                                         host_rgba8[v].data_ptr() if host_rgba8 is not None else 0)
                                for v in range(V)])
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
@@ -600,31 +613,6 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
                                           _stream_handle()))
     counters._g6r_keepalive = ws
     return images, counters
-
-
-def _balanced_slices(V: int, chunk: int):
-    """Split V views into ceil(V / chunk) contiguous slices of (almost) equal
-    size: 20 views at 16 become 10 + 10 instead of 16 + a 4-view tail."""
-    nb = max(1, -(-V // max(1, chunk)))
-    base, extra = divmod(V, nb)
-    out, k = [], 0
-    for i in range(nb):
-        step = base + (1 if i < extra else 0)
-        out.append(slice(k, k + step))
-        k += step
-    return out
-
-
-_LANES = {}
-
-
-def _render_lanes(dev):
-    """Two render streams and a copy stream per device, reused across calls."""
-    key = dev.index if dev.index is not None else torch.cuda.current_device()
-    lanes = _LANES.get(key)
-    if lanes is None:
-        lanes = _LANES[key] = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
-    return lanes
 
 
 def _host_mapped(t) -> bool:
@@ -640,11 +628,14 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     """Render many views to host memory: (V, H, W, 4) like stacking
     ``render(scene, cam)`` over ``cameras``.
 
-    Views are rendered ``batch`` per launch on two alternating streams and
-    each chunk's images are copied device->host into pinned memory on a side
-    stream while later chunks render (with G6R_ZERO_COPY=1 the compositor
-    writes the pinned host images itself instead).  One synchronisation at the end; views that overflowed the entry
-    capacity are re-rendered individually."""
+    One ``render_views`` call (``batch`` views per launch, consecutive batches
+    pipelined on two streams) whose frames carry page-locked host
+    destinations: the library copies each view device->host as soon as the
+    compositor has finished it (g6r_frame.host_image, gated on the device by
+    the view's completion flag), so the transfers overlap the rest of the
+    rendering and only the last view's copy trails the last kernel.  One
+    synchronisation at the end; views that overflowed the entry capacity are
+    re-rendered individually."""
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     cams = list(cameras)
@@ -653,44 +644,16 @@ def render_batch(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
         return np.zeros((0, 0, 0, 4), dtype=config.dtype())
     H, W = int(cams[0].height), int(cams[0].width)
     dt = torch.float32 if config.precision == "f32" else torch.float64
-    dev = prep.device
     # pinned output owned by the returned array (torch's caching host allocator
     # recycles the block once the array is released): no extra host copy
     host = torch.empty((V, H, W, 4), dtype=dt, pin_memory=True)
     chunk = max(1, min(int(batch), MAX_BATCH))
     if ZERO_COPY and _host_mapped(host):
-        # zero-copy: the compositor epilogue writes every finished pixel
-        # straight into the pinned host array over PCIe while the rest of the
-        # batch renders -- no device image, no copy after the render
+        # the compositor epilogue writes the pinned host array itself
         _, cnt = render_views(scene, cams, group_mask, config, out=host, concurrency=chunk)
-        cnt = cnt.cpu().numpy()   # synchronises: the kernels that wrote `host` are done
-        out = host.numpy()
-        for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
-            fr, _ = _render_checked(prep, bits, cams[v], config, False)
-            out[v] = fr.image.cpu().numpy()
-        return out
-    images = torch.empty((V, H, W, 4), dtype=dt, device=dev)
-    main = torch.cuda.current_stream()
-    lanes = _render_lanes(dev)
-    copy = lanes[2]
-    for ln in lanes:
-        ln.wait_stream(main)
-    counters = []
-    for i, sl in enumerate(_balanced_slices(V, chunk)):
-        lane = lanes[i & 1]
-        with torch.cuda.stream(lane):
-            _, cnt = render_views(scene, cams[sl], group_mask, config, out=images[sl],
-                                  concurrency=chunk)
-        counters.append(cnt)
-        ev = torch.cuda.Event()
-        ev.record(lane)
-        copy.wait_event(ev)
-        with torch.cuda.stream(copy):
-            host[sl].copy_(images[sl], non_blocking=True)
-    for ln in lanes:
-        main.wait_stream(ln)
-    copy.synchronize()
-    cnt = torch.cat([c.to(dev) for c in counters]).cpu().numpy()
+    else:
+        _, cnt = render_views(scene, cams, group_mask, config, concurrency=chunk, host_out=host)
+    cnt = cnt.cpu().numpy()   # synchronises: kernels and host copies are done
     out = host.numpy()
     for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
         fr, _ = _render_checked(prep, bits, cams[v], config, False)
@@ -718,21 +681,10 @@ def render_frames_u8(scene, cameras, background=(0.0, 0.0, 0.0), group_mask=None
     frames = torch.empty((V, H, W, 4), dtype=torch.uint8, device=dev)
     chunk = max(1, min(int(batch), MAX_BATCH))
     host = None if device_out else torch.empty((V, H, W, 4), dtype=torch.uint8, pin_memory=True)
-    main = torch.cuda.current_stream()
-    copy = torch.cuda.Stream(device=dev)
-    counters = []
-    for sl in _balanced_slices(V, chunk):
-        _, cnt = render_views(scene, cams[sl], group_mask, config, concurrency=chunk,
-                              rgba8=frames[sl], background=background, image=False)
-        counters.append(cnt)
-        if host is not None:
-            ev = torch.cuda.Event()
-            ev.record(main)
-            copy.wait_event(ev)
-            with torch.cuda.stream(copy):
-                host[sl].copy_(frames[sl], non_blocking=True)
-                frames[sl].record_stream(copy)
-    cnt = torch.cat(counters).cpu().numpy()   # synchronises the render stream
+    # each view's frame is copied to `host` as soon as it is complete
+    _, cnt = render_views(scene, cams, group_mask, config, concurrency=chunk, rgba8=frames,
+                          background=background, image=False, host_rgba8=host)
+    cnt = cnt.cpu().numpy()   # synchronises: kernels and host copies are done
     for v in np.nonzero(cnt[:, nat.CNT_OVERFLOW])[0]:
         while True:   # re-render an overflowed view with a grown capacity
             prep.entry_hint = min(int(cnt[v, nat.CNT_ENTRIES] * 1.25) + 4096, (1 << 30) - 1)
@@ -744,12 +696,9 @@ def render_frames_u8(scene, cameras, background=(0.0, 0.0, 0.0), group_mask=None
                 break
             cnt[v] = c1[0]
         if host is not None:
-            copy.wait_stream(main)
-            with torch.cuda.stream(copy):
-                host[v].copy_(frames[v], non_blocking=True)
+            host[v].copy_(frames[v])
     if host is None:
         return frames
-    copy.synchronize()
     return host.numpy()
 
 
