@@ -37,6 +37,17 @@ def test_library_loads_and_exports_every_header_symbol():
     assert "sm_100a" in nat.version()
 
 
+def test_frame_struct_matches_header():
+    """ctypes g6r_frame mirrors include/g6r.h field for field (the host-copy
+    pointers sit after the background colour)."""
+    text = open(os.path.join(ROOT, "include", "g6r.h")).read()
+    body = text[text.index("typedef struct g6r_frame {"):text.index("} g6r_frame;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"\**\s*([a-z_0-9]+)(?:\[\d+\])?;", body)
+    assert names == [f[0] for f in nat.Frame._fields_]
+    assert ctypes.sizeof(nat.Frame) == 7 * 8 + 3 * 8 + 2 * 8
+
+
 def test_workspace_size_grows_with_capacity():
     lib = nat.load()
     a = lib.g6r_workspace_bytes(1000, 64, 1 << 16, 0)
