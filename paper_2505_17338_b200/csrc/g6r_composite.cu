@@ -21,7 +21,7 @@
 namespace g6r {
 
 #ifndef G6R_GROUPED_MINB
-#define G6R_GROUPED_MINB 9   // min CTAs/SM for the grouped f32 compositor (<= 56 registers)
+#define G6R_GROUPED_MINB 8   // min CTAs/SM for the grouped f32 compositor (<= 64 registers)
 #endif
 #ifndef G6R_SCHED_MINB
 #define G6R_SCHED_MINB 0   // min CTAs/SM for the scheduled f32 compositor (A/B knob)

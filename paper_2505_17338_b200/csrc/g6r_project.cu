@@ -350,8 +350,11 @@ __device__ __forceinline__ void depth_extrema(bool kept, unsigned db, unsigned *
 // kSplatKeys (hot path, unordered): no tile entries at all -- every scene row
 // writes one depth key (f32 depth bits, all-ones for rows not drawn) and its
 // tile rect, for the splat-level sort in g6r_tiles.cu.
+#ifndef G6R_PROJ_MINB
+#define G6R_PROJ_MINB 4   // CTAs per SM the projection is compiled for (A/B knob)
+#endif
 template <bool kF64, bool kOrdered, bool kSplatKeys = false>
-__global__ void __launch_bounds__(kBlock, 4)
+__global__ void __launch_bounds__(kBlock, G6R_PROJ_MINB)
 k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_splat_out so,
           int write_entries, double sh_c0, double sh_c1) {
     __shared__ int s_tile;
