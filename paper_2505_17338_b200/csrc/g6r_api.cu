@@ -43,7 +43,7 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
     size_t internal, hist, proj, clear_end, tile_starts, payload, keys0, keys1, vals0, vals1,
-        sort_counts, rect, chunk_hist, warp_prefix, tile_total, sched, done, total;
+        sort_counts, rect, crect, chunk_hist, warp_prefix, tile_total, sched, done, total;
     int64_t sort_tiles_cap, nrows;
 };
 
@@ -78,6 +78,8 @@ static Layout layout(int64_t n, int64_t tiles, int64_t cap, int precision) {
     o = align_up(o + (size_t)kMaxPasses * L.sort_tiles_cap * kBins * sizeof(unsigned));
     L.rect = o;
     o = align_up(o + (size_t)n * sizeof(uint2));
+    L.crect = o;
+    o = align_up(o + (size_t)n * sizeof(uint2));
     L.chunk_hist = o;
     o = align_up(o + (size_t)ceil_div(n > 0 ? n : 1, chunk_splats(tiles)) * tiles * sizeof(unsigned));
     L.warp_prefix = o;   // kScatterWarps x ceil(T/2) packed words per chunk
@@ -108,6 +110,7 @@ static Workspace carve(void *base, const Layout &L, int64_t cap) {
     w.vals[1] = reinterpret_cast<unsigned *>(b + L.vals1);
     w.sort_counts = reinterpret_cast<unsigned *>(b + L.sort_counts);
     w.rect = reinterpret_cast<uint2 *>(b + L.rect);
+    w.crect = reinterpret_cast<uint2 *>(b + L.crect);
     w.chunk_hist = reinterpret_cast<unsigned *>(b + L.chunk_hist);
     w.warp_prefix = reinterpret_cast<unsigned *>(b + L.warp_prefix);
     w.tile_total = reinterpret_cast<unsigned *>(b + L.tile_total);

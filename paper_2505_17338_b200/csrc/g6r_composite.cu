@@ -254,6 +254,18 @@ __device__ __forceinline__ void signal_view_done(const Batch &bt, int view, int 
     }
 }
 
+#ifdef G6R_CTA_TRACE
+// Debug build only (-DG6R_CTA_TRACE): per compositor CTA (globaltimer start,
+// end, SM, view << 16 | item, run length), read by g6r_debug_cta_trace.
+__device__ unsigned long long g_cta_trace[1 << 17][4];
+__device__ unsigned g_cta_trace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // One CTA per tile, one thread per pixel.  kNB > 0: compile-time block size
 // (16x16 tiles, static shared memory); kNB == 0: any tile size up to 32x32.
 //
@@ -328,6 +340,9 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         w.inside = w.px < v.iw && w.py < v.ih;
         return w;
     };
+#ifdef G6R_CTA_TRACE
+    const unsigned long long t_start = gtimer();
+#endif
     const Where at = where();
     const int view = at.view;
     const ViewParams &vp = bt.vp[view];
@@ -642,6 +657,20 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
         if (last_contrib) last_contrib[p] = last;
     }
     if (bt.signal) signal_view_done(bt, fin.view, kSub);
+#ifdef G6R_CTA_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned k = atomicAdd(&g_cta_trace_n, 1u);
+        if (k < (1u << 17)) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            g_cta_trace[k][0] = t_start;
+            g_cta_trace[k][1] = gtimer();
+            g_cta_trace[k][2] = ((unsigned long long)smid << 32) | (unsigned)(fin.view << 16 | (fin.tile * kSub + (fin.band ? 1 : 0)));
+            g_cta_trace[k][3] = (unsigned long long)(bt.ws[fin.view].tile_starts[fin.tile + 1] - bt.ws[fin.view].tile_starts[fin.tile]);
+        }
+    }
+#endif
 }
 
 // Compositor work order for a batch: every (view, tile) item ranked by its run
@@ -867,6 +896,18 @@ __global__ void k_debug_exp(int64_t n, const double *x, double *y) {
          i += (int64_t)gridDim.x * blockDim.x)
         y[i] = exp_glibc(x[i], s_tab);
 }
+
+#ifdef G6R_CTA_TRACE
+extern "C" int g6r_debug_cta_trace(unsigned long long *host, int max_rows) {
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, g_cta_trace_n, sizeof n);
+    const int rows = (int)std::min<unsigned>(n, (unsigned)max_rows);
+    if (rows > 0) cudaMemcpyFromSymbol(host, g_cta_trace, (size_t)rows * 32);
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(g_cta_trace_n, &zero, sizeof zero);
+    return rows;
+}
+#endif
 
 int launch_debug_exp(int64_t n, const double *x, double *y, cudaStream_t st) {
     if (n == 0) return G6R_OK;

@@ -28,6 +28,8 @@ struct Workspace {
     int64_t *tile_starts;           // T+1 (internal copy)
     int4 *splat_rect;               // optional (backward): per splat (entry offset, x0, y0, wx)
     uint2 *rect;                    // splat-sort path: per scene row (x0 | y0 << 16, wx | hy << 16)
+    uint2 *crect;                   // splat-sort path: the tiles of rect the compositor's cull box
+                                    // touches (runs without exports skip the other entries)
     unsigned *chunk_hist;           // splat-sort path: per chunk of sorted splats, T tile counts
     unsigned *warp_prefix;          // splat-sort path: per chunk, per scatter warp, packed u16 tile offsets
     unsigned *tile_total;           // splat-sort path: T entry counts

@@ -455,10 +455,11 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
         m_base = s_pm;
         e_base = s_pe;
     }
+    float cex = 0.f, cey = 0.f;   // the payload's cull extents (reused for the culled rect)
     if (kept) {
         const long long m = kOrdered ? m_base + lm : i;
         if (kF64) {
-            float ex, ey;
+            float &ex = cex, &ey = cey;
             cull_extents(o.ca, o.cb, o.cc, 0x1p-52, ex, ey, o.alpha);
             PayloadF64 p;
             p.a = make_double2(o.u, o.v);
@@ -470,7 +471,7 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             reinterpret_cast<PayloadF64 *>(ws.payload)[m] = p;
         } else {
             const float fa = (float)o.ca, fb = (float)o.cb, fc = (float)o.cc;
-            float ex, ey;
+            float &ex = cex, &ey = cey;
             const float fal = (float)o.alpha;
             cull_extents_f32(fa, fb, fc, ex, ey, fal);
             PayloadF32 p;
@@ -510,6 +511,27 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
             ws.rect[i] = kept ? make_uint2((unsigned)x0 | ((unsigned)y0 << 16),
                                            (unsigned)wx | ((unsigned)hy << 16))
                               : make_uint2(0u, 0u);
+            // The tiles of the rect that the compositor's cull box touches:
+            // pixel columns [ceil(fl(mx - ex)), floor(fl(mx + ex))] -- the same
+            // float tests as the compositor's (g6r_composite.cu stage) --
+            // clipped to the image.  Entries outside it are never visited by
+            // any pixel, so runs without exported indices skip them.
+            uint2 cr = make_uint2(0u, 0u);
+            if (kept) {
+                const float ex = cex, ey = cey;
+                const float mxf = (float)o.u, myf = (float)o.v;
+                const int ts = vp.tile_size;
+                const int xl = max(__float2int_ru(mxf - ex), 0), xh = min(__float2int_rd(mxf + ex), vp.iw - 1);
+                const int yl = max(__float2int_ru(myf - ey), 0), yh = min(__float2int_rd(myf + ey), vp.ih - 1);
+                if (xl <= xh && yl <= yh) {
+                    const int cx0 = max(xl / ts, x0), cx1 = min(xh / ts, x0 + wx - 1);
+                    const int cy0 = max(yl / ts, y0), cy1 = min(yh / ts, y0 + hy - 1);
+                    if (cx0 <= cx1 && cy0 <= cy1)
+                        cr = make_uint2((unsigned)cx0 | ((unsigned)cy0 << 16),
+                                        (unsigned)(cx1 - cx0 + 1) | ((unsigned)(cy1 - cy0 + 1) << 16));
+                }
+            }
+            ws.crect[i] = cr;
         }
         __syncthreads();
         // this block's drawn count, for the optional export of the runs as

@@ -33,6 +33,7 @@ struct PartCtx {
     int chunk;             // sorted splats per chunk
     int tiles, tiles_x;
     const unsigned long long *items;   // depth-sorted (depth code << vbits | row)
+    const uint2 *rect;                 // tile rects the runs are built from
 };
 
 __device__ __forceinline__ bool part_ctx(const Batch &b, int v, PartCtx &c) {
@@ -45,6 +46,11 @@ __device__ __forceinline__ bool part_ctx(const Batch &b, int v, PartCtx &c) {
     c.chunk = chunk_splats(c.tiles);
     c.chunks = ceil_div(c.m, c.chunk);
     c.items = ws.keys[ws.internal[kSortPasses] & 1];
+    // runs that are exported (entry_splat / tile_starts) or indexed by
+    // last_contrib are the reference's; otherwise only the entries the
+    // compositor can visit (same pixels, same order: bit-identical images)
+    const ViewOut &o = b.out[v];
+    c.rect = (o.entry_splat || o.tile_starts || o.last_contrib || !ws.crect) ? ws.rect : ws.crect;
     return true;
 }
 
@@ -74,7 +80,7 @@ __device__ __forceinline__ EntryGroup load_group(const PartCtx &c, const Workspa
     g.ry = 0;
     if (sp < end) {
         g.row = (unsigned)(c.items[sp] & vmask);
-        const uint2 r = ws.rect[g.row];
+        const uint2 r = c.rect[g.row];
         g.rx = r.x;
         g.ry = r.y;
     }
@@ -129,7 +135,7 @@ k_chunk_count(const __grid_constant__ Batch b, unsigned long long vmask) {
     for (int64_t sp = w0s + lane; sp < w1s; sp += 32) {
         const unsigned row = (unsigned)(c.items[sp] & vmask);
         int x0, y0, wx, hy;
-        unpack_rect(ws.rect[row], x0, y0, wx, hy);
+        unpack_rect(c.rect[row], x0, y0, wx, hy);
         for (int yy = 0; yy < hy; ++yy)
             for (int xx = 0; xx < wx; ++xx) {
                 const int t = (y0 + yy) * c.tiles_x + x0 + xx;
