@@ -13,7 +13,7 @@
 //   k_chunk_scatter  per chunk: each warp recounts its slice of the chunk per
 //                    tile, the counts are prefixed over warps, then each warp
 //                    expands its splats' entries in order and ranks them with
-//                    match-any on the tile id against its running counters;
+//                    a ballot match on the tile id against its running counters;
 //                    every entry's splat row is written to tile_start + chunk
 //                    prefix + warp prefix + running count + rank.
 // Every step is deterministic and keeps the sorted order, so runs, tile starts
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const __grid_constant__ Batc
 // at k_chunk_count's per-warp prefix (16-bit counters, two per shared word);
 // tile_start + chunk prefix is kept per tile.  Each warp walks its splats in
 // groups of 32, enumerates the group's entries in order 32 at a time
-// (group_entry) and ranks them with match-any on the tile id against its own
+// (group_entry) and ranks them with a ballot match on the tile id against its own
 // running counters; the leader of each tile's peers advances the counter.  No
 // CTA barrier after the setup, and every position is a function of the sorted
 // order alone.
