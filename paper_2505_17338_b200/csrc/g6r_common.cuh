@@ -35,7 +35,10 @@ namespace g6r {
 
 constexpr int kBlock = 256;          // threads per CTA for streaming kernels
 constexpr int kMaxPasses = 8;        // radix passes (8-bit digits over <= 64-bit keys)
-constexpr int kSortItems = 8;        // keys per thread in a onesweep tile
+#ifndef G6R_SORT_ITEMS
+#define G6R_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = G6R_SORT_ITEMS;   // keys per thread in a onesweep tile
 constexpr int kSortThreads = 256;    // threads per onesweep CTA
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per tile
 constexpr double kMinAlpha = 1.0 / 255.0;        // raster.py:47

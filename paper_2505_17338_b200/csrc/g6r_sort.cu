@@ -239,7 +239,10 @@ constexpr int kOsWarps = kSortThreads / 32;
 // 8 warps rank their 256 keys each into per-warp 16-bit digit counters; each
 // thread then owns two digits for the prefix over warps, the status publish
 // and the look-back.
-__global__ void __launch_bounds__(kSortThreads, 4)
+#ifndef G6R_SORT_MINB
+#define G6R_SORT_MINB 4
+#endif
+__global__ void __launch_bounds__(kSortThreads, G6R_SORT_MINB)
 k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int64_t splat_n) {
     __shared__ unsigned s_goff[kBins];
     __shared__ unsigned short s_wh[kOsWarps][kBins];
