@@ -524,8 +524,12 @@ k_project(g6r_scene scene, uint32_t mask, const __grid_constant__ Batch b, g6r_s
                 const int xl = max(__float2int_ru(mxf - ex), 0), xh = min(__float2int_rd(mxf + ex), vp.iw - 1);
                 const int yl = max(__float2int_ru(myf - ey), 0), yh = min(__float2int_rd(myf + ey), vp.ih - 1);
                 if (xl <= xh && yl <= yh) {
-                    const int cx0 = max(xl / ts, x0), cx1 = min(xh / ts, x0 + wx - 1);
-                    const int cy0 = max(yl / ts, y0), cy1 = min(yh / ts, y0 + hy - 1);
+                    // pixel -> tile (non-negative): a shift for power-of-two tiles
+                    const bool pow2 = (ts & (ts - 1)) == 0;
+                    const int sh = __ffs(ts) - 1;
+                    auto tdiv = [&](int p) { return pow2 ? p >> sh : p / ts; };
+                    const int cx0 = max(tdiv(xl), x0), cx1 = min(tdiv(xh), x0 + wx - 1);
+                    const int cy0 = max(tdiv(yl), y0), cy1 = min(tdiv(yh), y0 + hy - 1);
                     if (cx0 <= cx1 && cy0 <= cy1)
                         cr = make_uint2((unsigned)cx0 | ((unsigned)cy0 << 16),
                                         (unsigned)(cx1 - cx0 + 1) | ((unsigned)(cy1 - cy0 + 1) << 16));
