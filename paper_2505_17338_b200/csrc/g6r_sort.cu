@@ -63,16 +63,22 @@ __device__ __forceinline__ bool entries_valid(const int64_t *counters, int64_t c
 // (dmin, dbits, passes) of a view from the projection's depth-bit extrema.
 // With `sentinel` (splat sort) one more code, span + 1, is reserved for rows
 // that were not drawn (key all-ones), so they sort after every drawn splat.
+// Digit width: the fewest passes of at most kRadixBits bits, then the
+// narrowest digit that still covers the key in that many passes (a 23-bit key
+// runs as 3 x 8 bits, not 3 x 9): fewer bins make every tile's digit prefix,
+// status publication and look-back cheaper (1 digit per thread instead of 2).
 __device__ __forceinline__ void view_key_shape(const long long *internal, int tbits, bool sentinel,
                                                unsigned &dmin, unsigned &dtop, int &dbits,
-                                               int &passes) {
+                                               int &passes, int &rbits) {
     const unsigned lo = ~(unsigned)internal[kDepthMinInv];
     const unsigned hi = (unsigned)internal[kDepthMax];
     const unsigned span = hi >= lo ? hi - lo : 0u;
     dmin = hi >= lo ? lo : 0u;
     dtop = span + (sentinel ? 1u : 0u);   // largest compressed depth code
     dbits = dtop ? 32 - __clz(dtop) : 0;
-    passes = (tbits + dbits + kRadixBits - 1) / kRadixBits;
+    const int total = tbits + dbits;
+    passes = (total + kRadixBits - 1) / kRadixBits;
+    rbits = passes ? (total + passes - 1) / passes : kRadixBits;
 }
 
 __device__ __forceinline__ unsigned depth_code(unsigned long long key, unsigned dmin, unsigned dtop) {
@@ -81,10 +87,10 @@ __device__ __forceinline__ unsigned depth_code(unsigned long long key, unsigned 
 }
 
 __device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dmin, unsigned dtop,
-                                             int dbits, int shift) {
+                                             int dbits, int shift, unsigned mask) {
     const unsigned long long k2 =
         ((key >> 32) << dbits) | (unsigned long long)depth_code(key, dmin, dtop);
-    return (unsigned)(k2 >> shift) & (kBins - 1);
+    return (unsigned)(k2 >> shift) & mask;
 }
 
 // Common prologue: this view's entry count, key shape, and whether `pass` runs.
@@ -96,7 +102,8 @@ __device__ __forceinline__ unsigned digit_of(unsigned long long key, unsigned dm
 struct PassCtx {
     int64_t e, ntiles;
     unsigned dmin, dtop;
-    int dbits, passes, vbits;
+    int dbits, passes, vbits, rbits;   // rbits: digit width of this view's passes
+    unsigned nbins;                    // 1 << rbits (<= kBins)
     bool packed, splat;
 };
 
@@ -108,7 +115,8 @@ __device__ __forceinline__ bool pass_ctx(const Batch &b, int v, int tbits, int v
         c.e = splat_n;
         tbits = 0;
     }
-    view_key_shape(b.ws[v].internal, tbits, c.splat, c.dmin, c.dtop, c.dbits, c.passes);
+    view_key_shape(b.ws[v].internal, tbits, c.splat, c.dmin, c.dtop, c.dbits, c.passes, c.rbits);
+    c.nbins = 1u << c.rbits;
     c.ntiles = ceil_div(c.e, kSortTile);
     c.vbits = vbits;
     c.packed = tbits + c.dbits + vbits <= 64;
@@ -123,12 +131,11 @@ __device__ __forceinline__ unsigned long long pack_entry(unsigned long long key,
 
 __device__ __forceinline__ int pass_src(int pass) { return pass & 1; }
 
-// Lanes of the warp holding the same 10-bit value (9-bit digit or the kBins
-// "invalid" code): one ballot per bit instead of MATCH.ANY.
-__device__ __forceinline__ unsigned match_digit(unsigned d) {
+// Lanes of the warp holding the same (rbits+1)-bit value (digit, or the
+// nbins "invalid" code): one ballot per bit instead of MATCH.ANY.
+__device__ __forceinline__ unsigned match_digit(unsigned d, int rbits) {
     unsigned peers = 0xffffffffu;
-#pragma unroll
-    for (int bit = 0; bit <= kRadixBits; ++bit) {
+    for (int bit = 0; bit <= rbits; ++bit) {
         const bool on = (d >> bit) & 1u;
         const unsigned b = __ballot_sync(0xffffffffu, on);
         peers &= on ? b : ~b;
@@ -184,7 +191,8 @@ k_sort_hist(const __grid_constant__ Batch b, int tbits, int vbits, int64_t splat
             for (int q = 0; q < kH; ++q) {
                 if (i0 + (int64_t)q * blockDim.x >= c.e) break;
                 for (int p = 0; p < np; ++p)
-                    atomicAdd(&h[hw][p][digit_of(key[q], c.dmin, c.dtop, c.dbits, kRadixBits * (p0 + p))], 1u);
+                    atomicAdd(&h[hw][p][digit_of(key[q], c.dmin, c.dtop, c.dbits, c.rbits * (p0 + p),
+                                                  c.nbins - 1)], 1u);
             }
         }
         __syncthreads();
@@ -262,7 +270,8 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
     unsigned *status = ws.sort_counts + (int64_t)pass * ws.sort_tiles_cap * kBins;
     const unsigned *totals = ws.hist + pass * kBins;
     unsigned long long *ticket = reinterpret_cast<unsigned long long *>(&ws.internal[kTicketSortBase + pass]);
-    const int shift = kRadixBits * pass;
+    const int shift = c.rbits * pass;
+    const unsigned nbins = c.nbins, dmask = nbins - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kOwn = kBins / kSortThreads;   // digits per thread
     {   // global exclusive digit offsets: thread t owns digits kOwn*t ..
@@ -308,13 +317,13 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             const int64_t idx = base + k * 32 + lane;
-            const unsigned d = idx >= c.e ? (unsigned)kBins
-                               : c.packed ? (unsigned)(key[k] >> (c.vbits + shift)) & (kBins - 1)
-                                          : digit_of(key[k], c.dmin, c.dtop, c.dbits, shift);
-            const unsigned peers = match_digit(d);
+            const unsigned d = idx >= c.e ? nbins
+                               : c.packed ? (unsigned)(key[k] >> (c.vbits + shift)) & dmask
+                                          : digit_of(key[k], c.dmin, c.dtop, c.dbits, shift, dmask);
+            const unsigned peers = match_digit(d, c.rbits);
             const int leader = __ffs(peers) - 1;
             unsigned old = 0;
-            if (d < (unsigned)kBins && lane == leader) {
+            if (d < nbins && lane == leader) {
                 old = s_wh[warp][d];
                 s_wh[warp][d] = (unsigned short)(old + (unsigned)__popc(peers));
             }
@@ -327,6 +336,8 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
 #pragma unroll
         for (int q = 0; q < kOwn; ++q) {   // exclusive prefix over warps, publish
             const int d = tid + q * kSortThreads;
+            tot[q] = 0;
+            if ((unsigned)d >= nbins) continue;
             unsigned run = 0;
 #pragma unroll
             for (int w = 0; w < kOsWarps; ++w) {
@@ -340,6 +351,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
 #pragma unroll
         for (int q = 0; q < kOwn; ++q) {   // look back
             const int d = tid + q * kSortThreads;
+            if ((unsigned)d >= nbins) continue;
             unsigned excl = 0;
             if (tile > 0) {
                 excl = look_back(status, tile, d);
@@ -351,7 +363,7 @@ k_onesweep(const __grid_constant__ Batch b, int tbits, int vbits, int pass, int6
 #pragma unroll
         for (int k = 0; k < kSortItems; ++k) {
             const unsigned d = dr[k] >> 16;
-            if (d >= (unsigned)kBins) continue;
+            if (d >= nbins) continue;
             const unsigned pos = s_base[d] + s_wh[warp][d] + (dr[k] & 0xffffu);
             G6R_CHECK((int64_t)pos < c.e);
             kout[pos] = key[k];
