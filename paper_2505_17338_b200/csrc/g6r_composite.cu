@@ -542,6 +542,8 @@ k_composite(const __grid_constant__ Batch bt, int sorted) {
                             asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw * 1.44269504088896341f));
                             ai = al * e;
                             if (ok && ai < floor_hi && ai >= floor_lo) ai = al * splat_exp_s(pw, eops);
+                        } else if constexpr (sizeof(Real) == 8) {
+                            ai = al * exp_glibc(pw, s_tab64);   // libm exp, bit for bit
                         } else {
                             ai = al * splat_exp_s(pw, eops);
                         }
@@ -991,12 +993,21 @@ int launch_composite(const Batch &b, bool sorted, cudaStream_t st) {
         attrs_done.fetch_or(bit);
     }
     if (vp.precision) {
-        if (vp.tile_size == 16 && sched)
-            k_composite<double, 256 / kCompositeSub, kCompositeSub, false, true>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+        // f64 band kernels: grouped hit lists too (G6R_GROUPS64=1: one list per warp)
+        static const int groups64 = [] {
+            const char *e = getenv("G6R_GROUPS64");
+            return e ? atoi(e) : 8;
+        }();
+        const dim3 g2(grid.x * kCompositeSub, grid.y);
+        constexpr int nt = 256 / kCompositeSub;
+        if (vp.tile_size == 16 && sched && groups64 == 8)
+            k_composite<double, nt, kCompositeSub, false, true, 8><<<g2, nt, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16 && groups64 == 8)
+            k_composite<double, nt, kCompositeSub, false, false, 8><<<g2, nt, 0, st>>>(b, srt);
+        else if (vp.tile_size == 16 && sched)
+            k_composite<double, nt, kCompositeSub, false, true><<<g2, nt, 0, st>>>(b, srt);
         else if (vp.tile_size == 16)
-            k_composite<double, 256 / kCompositeSub, kCompositeSub>
-                <<<dim3(grid.x * kCompositeSub, grid.y), 256 / kCompositeSub, 0, st>>>(b, srt);
+            k_composite<double, nt, kCompositeSub><<<g2, nt, 0, st>>>(b, srt);
         else
             k_composite<double, 0><<<grid, threads, 2 * threads * (sizeof(Px<double>::S) + 4), st>>>(b, srt);
     } else {
