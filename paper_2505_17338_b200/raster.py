@@ -438,12 +438,14 @@ class DeviceFrame:
         self.capacity = capacity
 
 
-def _alloc_frame(camera, config, dev, with_state, cap, n, T):
+def _alloc_frame(camera, config, dev, with_state, cap, n, T, track=True):
     H, W = int(camera.height), int(camera.width)
     dt = torch.float32 if config.precision == "f32" else torch.float64
+    # track=False (image only): no final_t / last_contrib, so the runs may skip
+    # the entries no pixel can visit (g6r_tiles.cu part_ctx)
     fr = DeviceFrame(torch.empty((H, W, 4), dtype=dt, device=dev),
-                     torch.empty((H, W), dtype=dt, device=dev),
-                     torch.empty((H, W), dtype=torch.int32, device=dev),
+                     torch.empty((H, W), dtype=dt, device=dev) if track else None,
+                     torch.empty((H, W), dtype=torch.int32, device=dev) if track else None,
                      torch.empty(nat.NCOUNTERS, dtype=torch.int64, device=dev), capacity=cap)
     if with_state:
         m = max(n, 1)
@@ -460,7 +462,9 @@ def _alloc_frame(camera, config, dev, with_state, cap, n, T):
 
 
 def _frame_struct(fr: DeviceFrame) -> nat.Frame:
-    return nat.Frame(fr.image.data_ptr(), fr.final_t.data_ptr(), fr.last_contrib.data_ptr(),
+    return nat.Frame(fr.image.data_ptr(),
+                     fr.final_t.data_ptr() if fr.final_t is not None else 0,
+                     fr.last_contrib.data_ptr() if fr.last_contrib is not None else 0,
                      fr.counters.data_ptr(),
                      fr.entry_splat.data_ptr() if fr.entry_splat is not None else 0,
                      fr.tile_starts.data_ptr() if fr.tile_starts is not None else 0)
@@ -481,12 +485,12 @@ def _workspace(n, T, cap, precision, dev):
 
 
 def _launch(prep: ScenePrep, bits: int, camera, config: RenderConfig, with_state: bool,
-            cap: int) -> DeviceFrame:
+            cap: int, track: bool = True) -> DeviceFrame:
     cfg = _check_config(config)
     cam = _camera_struct(camera)
     tx, ty = _tiles(camera, cfg.tile_size)
     T = tx * ty
-    fr = _alloc_frame(camera, config, prep.device, with_state, cap, prep.n, T)
+    fr = _alloc_frame(camera, config, prep.device, with_state, cap, prep.n, T, track or with_state)
     ws, nbytes = _workspace(prep.n, T, cap, cfg.precision, prep.device)
     sc = prep.scene_struct()
     f = _frame_struct(fr)
@@ -740,7 +744,7 @@ def render(scene, camera, group_mask=None, config: RenderConfig = DEFAULT_CONFIG
     prep = prepare_scene(scene, config.w_mode)
     bits = _selection(prep, group_mask, config, RenderStats())
     while True:
-        fr = _launch(prep, bits, camera, config, False, int(prep.entry_hint))
+        fr = _launch(prep, bits, camera, config, False, int(prep.entry_hint), track=False)
         # image and counters come back in one synchronisation, via pinned memory
         img = torch.empty(fr.image.shape, dtype=fr.image.dtype, pin_memory=True)
         cnt = torch.empty(nat.NCOUNTERS, dtype=torch.int64, pin_memory=True)
