@@ -5,7 +5,6 @@
 // synchronises (except g6r_profiler_read, which waits on its own events).
 // Views are rendered in batches: every stage kernel takes up to kMaxBatch views
 // per launch (grid = work x views).
-#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -254,7 +253,6 @@ static WaitValue32Fn wait_value_fn() {
 
 static cudaStream_t g_copy[64];
 static std::mutex g_copy_mu;
-static std::vector<cudaEvent_t> g_copy_ev;   // G6R_DEBUG_COPY: one event per finished view copy
 static cudaStream_t copy_stream() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
@@ -327,22 +325,11 @@ static int enqueue_host_copies(const Batch &b, const g6r_frame *frames, const Co
             cudaEventDestroy(ev);
             evented = true;
         }
-        static const bool dbg = getenv("G6R_DEBUG_COPY") != nullptr;
-        if (dbg) fprintf(stderr, "g6r copy view %d: wait fn %p gated %d value %u\n", v, (void *)wait, (int)gated,
-                         b.out[v].done_value);
         const size_t px = (size_t)b.vp[v].iw * b.vp[v].ih;
         if (f.host_image && f.image)
             cudaMemcpyAsync(f.host_image, f.image, px * 4 * (b.vp[v].precision ? 8 : 4), cudaMemcpyDeviceToHost,
                             cc.cs);
         if (f.host_rgba8 && f.rgba8) cudaMemcpyAsync(f.host_rgba8, f.rgba8, px * 4, cudaMemcpyDeviceToHost, cc.cs);
-        if (dbg) {   // copy-done events, reported by g6r_trace_dump's debug twin below
-            cudaEvent_t ev;
-            if (cudaEventCreate(&ev) == cudaSuccess) {
-                cudaEventRecord(ev, cc.cs);
-                std::lock_guard<std::mutex> lock(g_copy_mu);
-                g_copy_ev.push_back(ev);
-            }
-        }
     }
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }
@@ -633,21 +620,6 @@ int g6r_host_device_pointer(void *host, void **device) {
         *device = nullptr;
         return fail(G6R_EINVAL, "pointer is not page-locked host memory mapped for the device");
     }
-    return G6R_OK;
-}
-
-// G6R_DEBUG_COPY probe: ms from `start` (an event the caller recorded) to
-// each recorded view copy's completion, printed to stderr, then cleared.
-extern "C" int g6r_debug_copy_times(void *start) {
-    std::lock_guard<std::mutex> lock(g_copy_mu);
-    for (size_t i = 0; i < g_copy_ev.size(); ++i) {
-        float ms = -1.f;
-        cudaEventSynchronize(g_copy_ev[i]);
-        if (start) cudaEventElapsedTime(&ms, (cudaEvent_t)start, g_copy_ev[i]);
-        fprintf(stderr, "g6r copy %zu done at %.3f ms\n", i, ms);
-        cudaEventDestroy(g_copy_ev[i]);
-    }
-    g_copy_ev.clear();
     return G6R_OK;
 }
 
