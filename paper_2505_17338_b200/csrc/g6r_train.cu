@@ -34,16 +34,29 @@ static void window_host(double *w) {
     for (int k = 0; k < kWin; ++k) w[k] /= s;
 }
 
-// planar channel c of an interleaved (H, W, C) image
-__global__ void k_extract(const double *__restrict__ img, int C, int c, int64_t hw,
-                          double *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = img[i * C + c];
+// The three colour channels of the MS-SSIM term are independent: every
+// per-channel kernel below takes its channel from blockIdx.y (blockIdx.z for
+// the correlation) and its planes `cs` doubles apart, so one launch covers the
+// channels with each channel's arithmetic unchanged.
+
+// planar channel c of the interleaved (H, W, 4) prediction and (H, W, tc) target
+__global__ void k_extract(const double *__restrict__ pred, const double *__restrict__ tgt, int tc,
+                          int64_t hw, double *__restrict__ x, double *__restrict__ y, int64_t cs) {
+    const int c = blockIdx.y;
+    x += c * cs;
+    y += c * cs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = pred[i * 4 + c];
+        y[i] = tgt[i * tc + c];
+    }
 }
 
 // 5 statistic planes x, y, x*x, y*y, x*y
 __global__ void k_products(const double *__restrict__ x, const double *__restrict__ y, int64_t hw,
-                           double *__restrict__ out) {
+                           double *__restrict__ out, int64_t cs) {
+    x += blockIdx.y * cs;
+    y += blockIdx.y * cs;
+    out += blockIdx.y * cs;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
         const double a = x[i], b = y[i];
         out[i] = a;
@@ -56,15 +69,18 @@ __global__ void k_products(const double *__restrict__ x, const double *__restric
 
 // 1-D correlation with the window along one axis of `planes` (h, w) planes.
 // valid: out length n - 10; full: n + 10 (zero padding, the adjoint).
-// grid (column blocks, output rows, planes): no index division; the taps are
-// summed in the same order as before (k ascending), so the result is unchanged
+// grid (column blocks, output rows, channels x planes): no index division in
+// the pixel loop; the taps are summed in order (k ascending)
 __global__ void k_corr1d(const double *__restrict__ in, double *__restrict__ out, int planes, int h,
-                         int w, int axis, int full) {
+                         int w, int axis, int full, int64_t cs) {
     const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
     const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
     const int shift = full ? kWin - 1 : 0;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, p = blockIdx.z;
-    if (j >= ow || i >= oh || p >= planes) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    const int c = blockIdx.z / planes, p = blockIdx.z - c * planes;
+    if (j >= ow || i >= oh) return;
+    in += c * cs;
+    out += c * cs;
     const double *src = in + (int64_t)p * h * w;
     double s = 0.0;
 #pragma unroll
@@ -79,12 +95,15 @@ __global__ void k_corr1d(const double *__restrict__ in, double *__restrict__ out
 static dim3 corr_grid(int planes, int h, int w, int axis, int full) {
     const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
     const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
-    return dim3((unsigned)((ow + 127) / 128), (unsigned)std::max(oh, 1), (unsigned)planes);
+    return dim3((unsigned)((ow + 127) / 128), (unsigned)std::max(oh, 1), (unsigned)(3 * planes));
 }
 
 // SSIM window maps (_ssim.py:66-84) from the 5 correlated statistics
-__global__ void k_ssim_maps(const double *__restrict__ st, int64_t n, double *__restrict__ maps) {
+__global__ void k_ssim_maps(const double *__restrict__ st, int64_t n, double *__restrict__ maps,
+                            int64_t cs) {
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    st += blockIdx.y * cs;
+    maps += blockIdx.y * cs;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double ux = st[i], uy = st[n + i], exx = st[2 * n + i], eyy = st[3 * n + i], exy = st[4 * n + i];
         const double sxx = exx - ux * ux, syy = eyy - uy * uy, sxy = exy - ux * uy;
@@ -100,9 +119,13 @@ __global__ void k_ssim_maps(const double *__restrict__ st, int64_t n, double *__
 }
 
 // deterministic partial sums: block b sums a fixed strided subset
+// (channel blockIdx.y: a, b `cs` doubles apart, partials kRedBlocks apart)
 __global__ void k_partials(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
-                           double *__restrict__ part) {
+                           double *__restrict__ part, int64_t cs) {
     __shared__ double s[256];
+    a += blockIdx.y * cs;
+    if (b) b += blockIdx.y * cs;
+    part += blockIdx.y * gridDim.x;
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         acc += b ? a[i] * b[i] : a[i];
@@ -115,18 +138,31 @@ __global__ void k_partials(const double *__restrict__ a, const double *__restric
     if (threadIdx.x == 0) part[blockIdx.x] = s[0];
 }
 
-__global__ void k_sum_partials(const double *__restrict__ part, int n, double *__restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < n; ++i) s += part[i];
-        *out = s;
+// ordered final sum of block b's n partials into out[b * ostride]: the
+// partials are staged in shared memory by the whole block (one memory round
+// trip instead of n dependent-latency loads), then summed by one thread in
+// index order
+__global__ void k_sum_partials(const double *__restrict__ part, int n, double *__restrict__ out,
+                               int ostride) {
+    __shared__ double s[kRedBlocks];
+    part += (int64_t)blockIdx.x * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = part[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += s[i];
+        out[(int64_t)blockIdx.x * ostride] = acc;
     }
 }
 
 // per-window gradients of SsimParts.backward (_ssim.py:86-98) for constant
 // per-window upstream gradients g_lcs, g_cs
+// (g_scale of channel c at g_scale[c * gstride])
 __global__ void k_ssim_bwd_maps(const double *__restrict__ maps, int64_t n, const double *g_scale,
-                                int last, double *__restrict__ gm) {
+                                int gstride, int last, double *__restrict__ gm, int64_t cs) {
+    maps += blockIdx.y * cs;
+    gm += blockIdx.y * cs;
+    g_scale += blockIdx.y * gstride;
     // per-window upstream gradient of this scale, computed on the device
     const double g_lcs = last ? *g_scale : 0.0, g_cs = last ? 0.0 : *g_scale;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -142,24 +178,38 @@ __global__ void k_ssim_bwd_maps(const double *__restrict__ maps, int64_t n, cons
 
 // g += adj(g_ux) + 2 x adj(g_exx) + y adj(g_exy)
 __global__ void k_ssim_bwd_combine(const double *__restrict__ adj, const double *__restrict__ x,
-                                   const double *__restrict__ y, int64_t hw, double *__restrict__ g) {
+                                   const double *__restrict__ y, int64_t hw, double *__restrict__ g,
+                                   int64_t cs) {
+    adj += blockIdx.y * cs;
+    x += blockIdx.y * cs;
+    y += blockIdx.y * cs;
+    g += blockIdx.y * cs;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
         g[i] += adj[i] + 2.0 * x[i] * adj[hw + i] + y[i] * adj[2 * hw + i];
 }
 
-// 2x2 average pooling (_ssim.py:47-51) and its adjoint (:54-62)
-__global__ void k_pool2(const double *__restrict__ in, int h, int w, double *__restrict__ out) {
+// 2x2 average pooling (_ssim.py:47-51) of x and y, and its adjoint (:54-62)
+__global__ void k_pool2(const double *__restrict__ x, const double *__restrict__ y, int h, int w,
+                        double *__restrict__ x2, double *__restrict__ y2, int64_t cs) {
     const int h2 = h / 2, w2 = w / 2;
+    x += blockIdx.y * cs;
+    y += blockIdx.y * cs;
+    x2 += blockIdx.y * cs;
+    y2 += blockIdx.y * cs;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)h2 * w2;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(q / w2), j = (int)(q % w2);
-        const double *r0 = in + (int64_t)(2 * i) * w + 2 * j, *r1 = r0 + w;
-        out[q] = 0.25 * (r0[0] + r1[0] + r0[1] + r1[1]);
+        const int64_t o = (int64_t)(2 * i) * w + 2 * j;
+        x2[q] = 0.25 * (x[o] + x[o + w] + x[o + 1] + x[o + w + 1]);
+        y2[q] = 0.25 * (y[o] + y[o + w] + y[o + 1] + y[o + w + 1]);
     }
 }
 
-__global__ void k_pool2_adjoint(const double *__restrict__ g2, int h, int w, double *__restrict__ out) {
+__global__ void k_pool2_adjoint(const double *__restrict__ g2, int h, int w, double *__restrict__ out,
+                                int64_t cs) {
     const int h2 = h / 2, w2 = w / 2;
+    g2 += blockIdx.y * cs;
+    out += blockIdx.y * cs;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)h * w;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(q / w), j = (int)(q % w);
@@ -180,8 +230,10 @@ __global__ void k_l1(const double *__restrict__ pred, const double *__restrict__
     }
 }
 
-__global__ void k_axpy_channel(const double *__restrict__ g, int64_t hw, int c, double alpha,
-                               double *__restrict__ grad) {
+__global__ void k_axpy_channel(const double *__restrict__ g, int64_t hw, double alpha,
+                               double *__restrict__ grad, int64_t cs) {
+    const int c = blockIdx.y;
+    g += c * cs;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
         grad[i * 4 + c] += alpha * g[i];
 }
@@ -247,8 +299,10 @@ static unsigned grid_for(int64_t n) {
 
 // --- host orchestration -------------------------------------------------------
 
+// x .. g: channel 0's planes; channel c's are c * cstride bytes further on
 struct LossLayout {
-    size_t x[5], y[5], maps[5], stats, tmp, gm, adj, g, part, scal, absd, in_pred, in_tgt, out_grad, total;
+    size_t x[5], y[5], maps[5], stats, tmp, gm, adj, g, cstride, part, scal, absd, in_pred, in_tgt,
+        out_grad, total;
 };
 
 static inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
@@ -280,8 +334,10 @@ static LossLayout loss_layout(int h, int w, int scales) {
     o = al(o + 3 * hw * 8);
     L.g = o;
     o = al(o + 2 * hw * 8);
+    L.cstride = o;
+    o *= 3;
     L.part = o;
-    o = al(o + kRedBlocks * 8);
+    o = al(o + 3 * kRedBlocks * 8);
     L.scal = o;
     o = al(o + 64 * 8);
     L.absd = o;
@@ -300,11 +356,12 @@ static LossLayout loss_layout(int h, int w, int scales) {
 
 size_t loss_workspace_bytes(int h, int w) { return loss_layout(h, w, 5).total; }
 
-// sum of a*b (or a) over n doubles into *out (device), deterministic
-static void dsum(const double *a, const double *b, int64_t n, double *part, double *out,
-                 cudaStream_t st) {
-    k_partials<<<kRedBlocks, 256, 0, st>>>(a, b, n, part);
-    k_sum_partials<<<1, 32, 0, st>>>(part, kRedBlocks, out);
+// sum of a*b (or a) over n doubles into *out (device), deterministic; for
+// nch channels (a, b `cs` doubles apart) into out[c * ostride]
+static void dsum(const double *a, const double *b, int64_t n, int nch, int64_t cs, double *part,
+                 double *out, int ostride, cudaStream_t st) {
+    k_partials<<<dim3(kRedBlocks, nch), 256, 0, st>>>(a, b, n, part, cs);
+    k_sum_partials<<<nch, 256, 0, st>>>(part, kRedBlocks, out, ostride);
 }
 
 // Scalar slots of the loss workspace (device doubles).
@@ -318,8 +375,9 @@ struct ScaleWeights {
 // MS-SSIM value and per-scale window gradients of one channel (_ssim.py:163-198):
 // terms = means (clamped at 0 for the multi-scale product), value = prod(terms^w),
 // g[j] = value * w_j / terms_j / count_j (0 where the reference skips the scale).
-__global__ void k_msssim_scalars(double *chan, int ns, ScaleWeights sw) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void k_msssim_scalars(double *chan, int ns, ScaleWeights sw) {   // block c: channel c
+    if (threadIdx.x != 0) return;
+    chan += blockIdx.x * kChanStride;
     double terms[5];
     for (int j = 0; j < ns; ++j) terms[j] = chan[j] / sw.count[j];
     double *g = chan + 6;
@@ -367,7 +425,7 @@ static void loss_launch(const double *pred, const double *tgt, int tc, int h, in
     // L1 (diffrender.py:126-129)
     double *absd = reinterpret_cast<double *>(base + L.absd);
     k_l1<<<grid_for(hw * 3), 256, 0, st>>>(pred, tgt, tc, hw, lambda_l1 / (double)(hw * 3), grad, absd);
-    dsum(absd, nullptr, hw * 3, part, scal + kSlotL1, st);
+    dsum(absd, nullptr, hw * 3, 1, 0, part, scal + kSlotL1, 0, st);
     if (lambda_ssim > 0.0) {
         // effective_scales (_ssim.py:116-120)
         const int ns = std::min(h, w) < (1 << (scales - 1)) * kWin ? 1 : scales;
@@ -384,59 +442,57 @@ static void loss_launch(const double *pred, const double *tgt, int tc, int h, in
         }
         for (int j = 0; j < ns; ++j)
             sw.count[j] = (double)((int64_t)(hs[j] - kWin + 1) * (wsz[j] - kWin + 1));
-        for (int c = 0; c < 3; ++c) {
-            double *chan = scal + kSlotChan + c * kChanStride;
-            double *xs[5], *ys[5], *mp[5];
-            for (int j = 0; j < ns; ++j) {
-                xs[j] = reinterpret_cast<double *>(base + L.x[j]);
-                ys[j] = reinterpret_cast<double *>(base + L.y[j]);
-                mp[j] = reinterpret_cast<double *>(base + L.maps[j]);
-            }
-            k_extract<<<grid_for(hw), 256, 0, st>>>(pred, 4, c, hw, xs[0]);
-            k_extract<<<grid_for(hw), 256, 0, st>>>(tgt, tc, c, hw, ys[0]);
-            for (int j = 0; j < ns; ++j) {
-                const int hj = hs[j], wj = wsz[j];
-                const int64_t hwj = (int64_t)hj * wj;
-                const int hv = hj - kWin + 1, wv = wj - kWin + 1;
-                const int64_t nv = (int64_t)hv * wv;
-                double *stats = reinterpret_cast<double *>(base + L.stats);
-                double *tmp = reinterpret_cast<double *>(base + L.tmp);
-                k_products<<<grid_for(hwj), 256, 0, st>>>(xs[j], ys[j], hwj, stats);
-                k_corr1d<<<corr_grid(5, hj, wj, 0, 0), 128, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0);
-                k_corr1d<<<corr_grid(5, hv, wj, 1, 0), 128, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0);
-                k_ssim_maps<<<grid_for(nv), 256, 0, st>>>(stats, nv, mp[j]);
-                if (j == ns - 1) dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, part, chan + j, st);
-                else dsum(mp[j] + 5 * nv, nullptr, nv, part, chan + j, st);
-                if (j + 1 < ns) {
-                    k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(xs[j], hj, wj, xs[j + 1]);
-                    k_pool2<<<grid_for(hwj / 4 + 1), 256, 0, st>>>(ys[j], hj, wj, ys[j + 1]);
-                }
-            }
-            k_msssim_scalars<<<1, 32, 0, st>>>(chan, ns, sw);
-            // backward from the coarsest scale (_ssim.py:175-198)
-            double *g = reinterpret_cast<double *>(base + L.g);
-            double *g2 = g + hw;
-            cudaMemsetAsync(g, 0, (size_t)hs[ns - 1] * wsz[ns - 1] * 8, st);
-            for (int j = ns - 1; j >= 0; --j) {
-                const int hj = hs[j], wj = wsz[j];
-                const int64_t hwj = (int64_t)hj * wj;
-                const int hv = hj - kWin + 1, wv = wj - kWin + 1;
-                const int64_t nv = (int64_t)hv * wv;
-                if (j < ns - 1) {   // upsample the coarser gradient into this level
-                    k_pool2_adjoint<<<grid_for(hwj), 256, 0, st>>>(g, hj, wj, g2);
-                    std::swap(g, g2);
-                }
-                double *gm = reinterpret_cast<double *>(base + L.gm);
-                double *tmp = reinterpret_cast<double *>(base + L.tmp);
-                double *adj = reinterpret_cast<double *>(base + L.adj);
-                k_ssim_bwd_maps<<<grid_for(nv), 256, 0, st>>>(mp[j], nv, chan + 6 + j, j == ns - 1, gm);
-                k_corr1d<<<corr_grid(3, hv, wv, 0, 1), 128, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1);
-                k_corr1d<<<corr_grid(3, hj, wv, 1, 1), 128, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1);
-                k_ssim_bwd_combine<<<grid_for(hwj), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g);
-            }
-            // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
-            k_axpy_channel<<<grid_for(hw), 256, 0, st>>>(g, hw, c, -lambda_ssim / 3.0, grad);
+        // all three channels per launch (grid y / z), channel c's planes cs doubles on
+        const int64_t cs = (int64_t)(L.cstride / 8);
+        double *chan = scal + kSlotChan;   // channel c's scalars kChanStride further on
+        double *xs[5], *ys[5], *mp[5];
+        for (int j = 0; j < ns; ++j) {
+            xs[j] = reinterpret_cast<double *>(base + L.x[j]);
+            ys[j] = reinterpret_cast<double *>(base + L.y[j]);
+            mp[j] = reinterpret_cast<double *>(base + L.maps[j]);
         }
+        double *stats = reinterpret_cast<double *>(base + L.stats);
+        double *tmp = reinterpret_cast<double *>(base + L.tmp);
+        k_extract<<<dim3(grid_for(hw), 3), 256, 0, st>>>(pred, tgt, tc, hw, xs[0], ys[0], cs);
+        for (int j = 0; j < ns; ++j) {
+            const int hj = hs[j], wj = wsz[j];
+            const int64_t hwj = (int64_t)hj * wj;
+            const int hv = hj - kWin + 1, wv = wj - kWin + 1;
+            const int64_t nv = (int64_t)hv * wv;
+            k_products<<<dim3(grid_for(hwj), 3), 256, 0, st>>>(xs[j], ys[j], hwj, stats, cs);
+            k_corr1d<<<corr_grid(5, hj, wj, 0, 0), 128, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0, cs);
+            k_corr1d<<<corr_grid(5, hv, wj, 1, 0), 128, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0, cs);
+            k_ssim_maps<<<dim3(grid_for(nv), 3), 256, 0, st>>>(stats, nv, mp[j], cs);
+            if (j == ns - 1) dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, 3, cs, part, chan + j, kChanStride, st);
+            else dsum(mp[j] + 5 * nv, nullptr, nv, 3, cs, part, chan + j, kChanStride, st);
+            if (j + 1 < ns)
+                k_pool2<<<dim3(grid_for(hwj / 4 + 1), 3), 256, 0, st>>>(xs[j], ys[j], hj, wj, xs[j + 1],
+                                                                       ys[j + 1], cs);
+        }
+        k_msssim_scalars<<<3, 32, 0, st>>>(chan, ns, sw);
+        // backward from the coarsest scale (_ssim.py:175-198)
+        double *g = reinterpret_cast<double *>(base + L.g);
+        double *g2 = g + hw;
+        cudaMemset2DAsync(g, L.cstride, 0, (size_t)hs[ns - 1] * wsz[ns - 1] * 8, 3, st);
+        double *gm = reinterpret_cast<double *>(base + L.gm);
+        double *adj = reinterpret_cast<double *>(base + L.adj);
+        for (int j = ns - 1; j >= 0; --j) {
+            const int hj = hs[j], wj = wsz[j];
+            const int64_t hwj = (int64_t)hj * wj;
+            const int hv = hj - kWin + 1, wv = wj - kWin + 1;
+            const int64_t nv = (int64_t)hv * wv;
+            if (j < ns - 1) {   // upsample the coarser gradient into this level
+                k_pool2_adjoint<<<dim3(grid_for(hwj), 3), 256, 0, st>>>(g, hj, wj, g2, cs);
+                std::swap(g, g2);
+            }
+            k_ssim_bwd_maps<<<dim3(grid_for(nv), 3), 256, 0, st>>>(mp[j], nv, chan + 6 + j, kChanStride,
+                                                                  j == ns - 1, gm, cs);
+            k_corr1d<<<corr_grid(3, hv, wv, 0, 1), 128, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1, cs);
+            k_corr1d<<<corr_grid(3, hj, wv, 1, 1), 128, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1, cs);
+            k_ssim_bwd_combine<<<dim3(grid_for(hwj), 3), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g, cs);
+        }
+        // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
+        k_axpy_channel<<<dim3(grid_for(hw), 3), 256, 0, st>>>(g, hw, -lambda_ssim / 3.0, grad, cs);
     }
     k_loss_parts<<<1, 32, 0, st>>>(scal, lambda_ssim > 0.0, lambda_l1, lambda_ssim, (double)(hw * 3));
 }
