@@ -23,6 +23,8 @@ namespace g6r {
 #define G6R_BWD_BATCH 64
 #endif
 constexpr int kBwdBatch = G6R_BWD_BATCH;   // entries staged per backward batch
+constexpr int kBwdWords = kBwdBatch / 32;     // hit-mask words per warp and batch
+static_assert(kBwdBatch % 32 == 0 && kBwdBatch <= 128, "batch: whole warps, one entry per thread");
 
 struct BwdSplat {
     double mx, my, ca, cb, cc, alpha, r, g, b;
@@ -31,6 +33,9 @@ struct BwdSplat {
 // Two CTAs per tile, one per 16x8 band (8x4 warp blocks, as the forward), one
 // thread per pixel; each band sweeps the run back to front from its own largest
 // last_contrib and writes its own row per entry (egrad + band * cap * 9).
+// Each warp walks only the batch entries whose footprint meets its 8x4 block
+// (a ballot of the staged masks, set bits in ascending order: the entry order
+// of the sweep), and records which of them it gave a nonzero row.
 __constant__ unsigned long long c_bwd_exp_tab[256] = G6R_EXP_TABLE;
 
 __global__ void __launch_bounds__(128)
@@ -44,7 +49,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
     __shared__ unsigned s_mask[kBwdBatch];
     __shared__ double s_part[4][kBwdBatch][9];
     __shared__ double s_red[4][9][33];   // per-warp transpose of the 9 partials
-    __shared__ unsigned char s_hit[4][kBwdBatch];
+    __shared__ unsigned s_rowm[4][kBwdWords];   // per warp: entries with a nonzero row
     __shared__ float4 s_wbox[4];
     __shared__ int s_maxlast;
     __shared__ unsigned long long s_etab[256];   // glibc exp table (g6r_common.cuh)
@@ -106,11 +111,18 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             s_mask[j] = mk;
         }
         __syncthreads();
-        for (int j = 0; j < cnt; ++j) {
+        unsigned hitw[kBwdWords], rowm[kBwdWords];
+#pragma unroll
+        for (int q = 0; q < kBwdWords; ++q) {
+            const int j = q * 32 + lane;
+            hitw[q] = __ballot_sync(0xffffffffu, j < cnt && ((s_mask[j] >> warp) & 1u));
+            rowm[q] = 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kBwdWords; ++q) while (hitw[q]) {   // warp-uniform: the entries some pixel of this warp may reach
+            const int j = q * 32 + __ffs(hitw[q]) - 1;
+            hitw[q] &= hitw[q] - 1u;
             const int64_t e = b1 - 1 - j;
-            const bool hit = (s_mask[j] >> warp) & 1u;
-            if (lane == 0) s_hit[warp][j] = hit;
-            if (!hit) continue;   // warp-uniform: no pixel of this warp can reach e
             double c[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) c[k] = 0.0;
@@ -146,10 +158,8 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                     }
                 }
             }
-            if (!__any_sync(0xffffffffu, contrib)) {   // an exact zero row: skip the reduction
-                if (lane == 0) s_hit[warp][j] = 0;
-                continue;
-            }
+            if (!__any_sync(0xffffffffu, contrib)) continue;   // an exact zero row: no reduction
+            rowm[q] |= 1u << (j & 31);
             // transpose through shared memory: lane 3k+p sums 11 (p < 2) or 10
             // lanes' values of component k in lane order, then p = 0 adds the
             // other two parts -- a fixed order (deterministic), ~40 issue slots
@@ -171,15 +181,34 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             if (lane < 27 && rp == 0) s_part[warp][j][rk] = (part + p1) + p2;
             __syncwarp();
         }
+        if (lane < kBwdWords) {
+            unsigned v = rowm[0];
+#pragma unroll
+            for (int q = 1; q < kBwdWords; ++q)
+                if (lane == q) v = rowm[q];
+            s_rowm[warp][lane] = v;
+        }
         __syncthreads();
         for (int q = threadIdx.x; q < cnt * 9; q += blockDim.x) {   // warps in index order
             const int j = q / 9, k = q % 9;
             double v = 0.0;
             for (int w = 0; w < 4; ++w)
-                if (s_hit[w][j]) v += s_part[w][j][k];
+                if ((s_rowm[w][j >> 5] >> (j & 31)) & 1u) v += s_part[w][j][k];
             egrad[(int64_t)s_orig[j] * 9 + k] = v;
         }
         __syncthreads();
+    }
+}
+
+// Zero both bands' rows of the view's entries (slots [0, entries)): rows the
+// sweep never reaches stay zero; the rest are overwritten.
+__global__ void k_zero_rows(const int64_t *counters, int64_t cap, double *__restrict__ egrad) {
+    const int64_t e = counters[G6R_CNT_ENTRIES];
+    const int64_t n = (e < cap ? e : cap) * 9;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        egrad[i] = 0.0;
+        egrad[cap * 9 + i] = 0.0;
     }
 }
 
@@ -452,13 +481,13 @@ int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspac
                     double *g_cov_raw, double *g_sh, double *g_opacity_raw, cudaStream_t st) {
     if (vp.tile_size != 16) return G6R_EINVAL;
     const int64_t n = scene.n;
-    cudaMemsetAsync(egrad, 0, (size_t)ws.entry_capacity * 9 * 2 * sizeof(double), st);
     cudaMemsetAsync(g_mu_p, 0, (size_t)n * 3 * sizeof(double), st);
     cudaMemsetAsync(g_mu_d, 0, (size_t)n * 3 * sizeof(double), st);
     cudaMemsetAsync(g_cov_raw, 0, (size_t)n * 21 * sizeof(double), st);
     cudaMemsetAsync(g_sh, 0, (size_t)n * 12 * sizeof(double), st);
     cudaMemsetAsync(g_opacity_raw, 0, (size_t)n * sizeof(double), st);
     if (n == 0) return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
+    k_zero_rows<<<148 * 4, 256, 0, st>>>(counters, ws.entry_capacity, egrad);
     k_composite_bwd<<<vp.tiles_x * vp.tiles_y * 2, 128, 0, st>>>(
         vp, static_cast<const PayloadF64 *>(ws.payload), ws.vals[0], ws.vals[1], ws.internal,
         ws.tile_starts, final_t, last, grad_image, ws.splat_rect, egrad, ws.entry_capacity);
