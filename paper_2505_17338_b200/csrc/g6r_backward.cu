@@ -231,9 +231,6 @@ __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
     for (int k = 0; k < 9; ++k) gsplat[m * 9 + k] = acc[k];
 }
 
-__constant__ int8_t c_tri_i[15] = {1, 2, 2, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 5};
-__constant__ int8_t c_tri_j[15] = {0, 1, 0, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4};
-
 struct BwdScene {
     const double *mu_p, *mu_d, *cov_raw, *sh;
     double ss[3], ds;
@@ -244,9 +241,12 @@ struct BwdOut {
     double *g_mu_p, *g_mu_d, *g_cov_raw, *g_sh, *g_opacity_raw;
 };
 
+#ifndef G6R_ROWS_MINB
+#define G6R_ROWS_MINB 3
+#endif
 // Chain one splat's 9 screen-space gradients to its 40 raw parameters
 // (diffrender.py:183-398, same intermediate names).
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, G6R_ROWS_MINB)
 k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, const int64_t *counters,
                 const int64_t *__restrict__ gids, const double *__restrict__ gsplat, BwdOut out,
                 double sh_c0, double sh_c1) {
@@ -401,7 +401,8 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, const int64_t *coun
     const double scale[6] = {sc.ss[0], sc.ss[1], sc.ss[2], sc.ds, sc.ds, sc.ds};
     const double *raw = sc.cov_raw + 21 * i;
     for (int k = 0; k < 6; ++k) L[k][k] = scale[k] * exp(raw[k]);
-    for (int k = 0; k < 15; ++k) L[c_tri_i[k]][c_tri_j[k]] = tanh(raw[6 + k]);
+#pragma unroll
+    for (int k = 0; k < 15; ++k) L[tril_i(k)][tril_j(k)] = tanh(raw[6 + k]);
     double pd[3][3];
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) {
@@ -452,8 +453,9 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, const int64_t *coun
         for (int p = 0; p < 6; ++p) gl += G[k][p] * L[p][k];
         g_raw[k] = gl * L[k][k];
     }
+#pragma unroll
     for (int k = 0; k < 15; ++k) {
-        const int a = c_tri_i[k], b = c_tri_j[k];
+        const int a = tril_i(k), b = tril_j(k);
         double gl = 0.0;
         for (int p = 0; p < 6; ++p) gl += G[a][p] * L[p][b];
         const double off = L[a][b];

@@ -33,6 +33,18 @@
 
 namespace g6r {
 
+// (row, column) of cov_raw[6 + k]: the row-major strict-lower pairs of the
+// 6x6 Cholesky factor (core.py:30-31: (1,0) (2,1) (2,0) (3,0..2) (4,0..3)
+// (5,0..4)); constexpr, so fully unrolled loops index registers, not local memory
+__host__ __device__ constexpr int tril_i(int k) {
+    return k < 1 ? 1 : k < 3 ? 2 : k < 6 ? 3 : k < 10 ? 4 : 5;
+}
+__host__ __device__ constexpr int tril_j(int k) {
+    return k == 1 ? 1 : k < 3 ? 0 : k < 6 ? k - 3 : k < 10 ? k - 6 : k - 10;
+}
+static_assert(tril_i(2) == 2 && tril_j(2) == 0 && tril_i(5) == 3 && tril_j(5) == 2 &&
+              tril_i(14) == 5 && tril_j(14) == 4, "tril order");
+
 constexpr int kBlock = 256;          // threads per CTA for streaming kernels
 constexpr int kMaxPasses = 8;        // radix passes (8-bit digits over <= 64-bit keys)
 #ifndef G6R_SORT_ITEMS

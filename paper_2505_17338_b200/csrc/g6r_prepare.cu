@@ -12,10 +12,6 @@
 
 namespace g6r {
 
-// row-major strict-lower pairs fixing the meaning of cov_raw[6:21] (core.py:30-31)
-__constant__ int8_t c_tril_i[15] = {1, 2, 2, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 5};
-__constant__ int8_t c_tril_j[15] = {0, 1, 0, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4};
-
 __device__ __forceinline__ void put_record(double2 *rec, int64_t n, int64_t i, const double *r44) {
 #pragma unroll
     for (int c = 0; c < G6R_REC_COLUMNS; ++c) rec[c * n + i] = make_double2(r44[2 * c], r44[2 * c + 1]);
@@ -50,7 +46,7 @@ k_prepare(int64_t n, const double *__restrict__ mu_p, const double *__restrict__
 #pragma unroll
         for (int d = 0; d < 6; ++d) L[d][d] = scale[d] * exp(raw[d]);
 #pragma unroll
-        for (int k = 0; k < 15; ++k) L[c_tril_i[k]][c_tril_j[k]] = tanh(raw[6 + k]);
+        for (int k = 0; k < 15; ++k) L[tril_i(k)][tril_j(k)] = tanh(raw[6 + k]);
 
         // Sigma[a][b] = ((p0+p2)+p4) + ((p1+p3)+p5), p_j = L[a][j] L[b][j]
         double S[6][6];

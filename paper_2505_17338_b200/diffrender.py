@@ -441,6 +441,10 @@ class DeviceTrainer:
         self.label_counts = torch.empty(32, dtype=torch.int64, device=self.dev)
         self.counters = torch.empty(nat.NCOUNTERS, dtype=torch.int64, device=self.dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # pinned landing buffers: the per-step label counts (degenerate policy)
+        # and forward counters (entry overflow) ride the loss's one read-back
+        self._h_label_counts = torch.empty(32, dtype=torch.int64).pin_memory()
+        self._h_counters = torch.empty(nat.NCOUNTERS, dtype=torch.int64).pin_memory()
         self.cap = max(1 << 20, 8 * n)
         self._ws = {}
         self._img = {}
@@ -476,10 +480,11 @@ class DeviceTrainer:
             _ptr(p["opacity_raw"]), _ptr(self.labels), ctypes.cast(self.ss, ctypes.c_void_p),
             self.directional_scale, self.w_mode, _ptr(self.records), _ptr(self.flags),
             _ptr(self.label_counts), _stream_handle()))
-        prep = ScenePrep(self.records, self.flags, self.label_counts.cpu().numpy(), self.n,
+        # the counts land on the host with the step's loss read-back; the
+        # degenerate policy is applied then (gradients()), before any update
+        self._h_label_counts.copy_(self.label_counts, non_blocking=True)
+        return ScenePrep(self.records, self.flags, self._h_label_counts.numpy(), self.n,
                          self.cfg.w_mode, self.dev)
-        _selection(prep, None, self.cfg, RenderStats())   # degenerate policy (raster.py:431-440)
-        return prep
 
     def step(self, view_index: int) -> dict:
         """One iteration on view ``view_index``; returns lr, l1, ssim_loss, total."""
@@ -502,12 +507,16 @@ class DeviceTrainer:
             nat.check(self.lib.g6r_backward_forward(
                 ctypes.byref(sc), 0xFFFF, ctypes.byref(camst), ctypes.byref(self.ccfg), _ptr(ws),
                 nbytes, self.cap, _ptr(self.counters), _ptr(image), stream))
-            c = self.counters.cpu().numpy()
+            self._h_counters.copy_(self.counters, non_blocking=True)
+            # one synchronising read-back per step: the loss scalars (the
+            # counters and label counts queued above arrive with them)
+            (total, l1, ssim_loss), _ = loss_device(image, target, self.loss_cfg, grad_out=gimg)
+            _selection(prep, None, self.cfg, RenderStats())   # degenerate policy (raster.py:431-440)
+            c = self._h_counters.numpy()
             if not c[nat.CNT_OVERFLOW]:
                 break
             self.cap = min(int(c[nat.CNT_ENTRIES] * 1.25) + 4096, (1 << 30) - 1)
         lr_now = self.lr()
-        (total, l1, ssim_loss), _ = loss_device(image, target, self.loss_cfg, grad_out=gimg)
         p, g = self.params, self.grads
         nat.check(self.lib.g6r_backward_apply(
             ctypes.byref(sc), ctypes.byref(camst), ctypes.byref(self.ccfg), _ptr(ws), nbytes,
