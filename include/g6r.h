@@ -72,6 +72,8 @@ enum {
     G6R_CNT_ENTRIES = 1,      /* E: tile entries (also when over capacity) */
     G6R_CNT_FATE = 2,         /* [2..7]: stage-code histogram 0..5 of selected rows */
     G6R_CNT_OVERFLOW = 8,     /* 1 if E exceeded entry_capacity (nothing sorted) */
+    G6R_CNT_GRAD_NONFINITE = 9, /* g6r_backward_apply / g6r_render_backward: 1 if any
+                                   gradient element written is not finite, else 0 */
     G6R_NCOUNTERS = 16
 };
 

@@ -31,6 +31,7 @@ CNT_DRAWN = 0
 CNT_ENTRIES = 1
 CNT_FATE = 2
 CNT_OVERFLOW = 8
+CNT_GRAD_NONFINITE = 9
 NCOUNTERS = 16
 NSTAGES = 4
 STAGE_NAMES = ("project", "sort", "ranges", "composite")

@@ -247,7 +247,7 @@ struct BwdOut {
 // Chain one splat's 9 screen-space gradients to its 40 raw parameters
 // (diffrender.py:183-398, same intermediate names).
 __global__ void __launch_bounds__(128, G6R_ROWS_MINB)
-k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, const int64_t *counters,
+k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
                 const int64_t *__restrict__ gids, const double *__restrict__ gsplat, BwdOut out,
                 double sh_c0, double sh_c1) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,20 +463,33 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, const int64_t *coun
     }
     for (int k = 0; k < 3; ++k) g_v3[k] += g_d[k];
     const double vdot = v[0] * g_v3[0] + v[1] * g_v3[1] + v[2] * g_v3[2];
+    double g_mp[3];
     for (int k = 0; k < 3; ++k) {
-        out.g_mu_p[3 * i + k] = g_madj[k] + (g_v3[k] - v[k] * vdot) * inv_dist;
+        g_mp[k] = g_madj[k] + (g_v3[k] - v[k] * vdot) * inv_dist;
+        out.g_mu_p[3 * i + k] = g_mp[k];
         out.g_mu_d[3 * i + k] = -g_d[k];
     }
     for (int k = 0; k < 21; ++k) out.g_cov_raw[21 * i + k] = g_raw[k];
     for (int k = 0; k < 12; ++k) out.g_sh[12 * i + k] = g_shv[k];
     out.g_opacity_raw[i] = g_opacity_raw;
+    // non-finite check of the 40 values written (the rows not written are
+    // zeros): the largest exponent field, all-ones only for inf / nan
+    unsigned ex = (unsigned)__double2hiint(g_opacity_raw) & 0x7ff00000u;
+    auto acc = [&](double x) { ex = max(ex, (unsigned)__double2hiint(x) & 0x7ff00000u); };
+    for (int k = 0; k < 3; ++k) {
+        acc(g_mp[k]);
+        acc(g_d[k]);
+    }
+    for (int k = 0; k < 21; ++k) acc(g_raw[k]);
+    for (int k = 0; k < 12; ++k) acc(g_shv[k]);
+    if (ex == 0x7ff00000u) counters[G6R_CNT_GRAD_NONFINITE] = 1;
 }
 
 static const double kShC0b = 0.28209479177387814;
 static const double kShC1b = 0.4886025119029199;
 
 int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspace &ws,
-                    const int64_t *counters, const double *final_t, const int32_t *last,
+                    int64_t *counters, const double *final_t, const int32_t *last,
                     const double *grad_image, const int64_t *gids, double *egrad, double *gsplat,
                     const double *mu_p, const double *mu_d, const double *cov_raw, const double *sh,
                     const double *ss, double ds, int w_mode, double *g_mu_p, double *g_mu_d,
@@ -488,6 +501,7 @@ int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspac
     cudaMemsetAsync(g_cov_raw, 0, (size_t)n * 21 * sizeof(double), st);
     cudaMemsetAsync(g_sh, 0, (size_t)n * 12 * sizeof(double), st);
     cudaMemsetAsync(g_opacity_raw, 0, (size_t)n * sizeof(double), st);
+    cudaMemsetAsync(counters + G6R_CNT_GRAD_NONFINITE, 0, sizeof(int64_t), st);
     if (n == 0) return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
     k_zero_rows<<<148 * 4, 256, 0, st>>>(counters, ws.entry_capacity, egrad);
     k_composite_bwd<<<vp.tiles_x * vp.tiles_y * 2, 128, 0, st>>>(

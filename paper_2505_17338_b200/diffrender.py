@@ -489,7 +489,7 @@ class DeviceTrainer:
     def step(self, view_index: int) -> dict:
         """One iteration on view ``view_index``; returns lr, l1, ssim_loss, total."""
         row = self.gradients(view_index)
-        self._adam()
+        self._adam(fused_check=True)
         return row
 
     def gradients(self, view_index: int) -> dict:
@@ -529,13 +529,17 @@ class DeviceTrainer:
         """Adam on ``self.grads`` (skipped when any is non-finite)."""
         self._adam()
 
-    def _adam(self):
-        self.flag.zero_()
+    def _adam(self, fused_check: bool = False):
         stream = _stream_handle()
-        for k in PARAM_GROUPS:
-            nat.check(self.lib.g6r_any_nonfinite(self.params[k].numel(), _ptr(self.grads[k]),
-                                                 _ptr(self.flag), stream))
-        if int(self.flag.item()):
+        if fused_check:   # the backward flagged non-finite gradients as it wrote them
+            bad = int(self.counters[nat.CNT_GRAD_NONFINITE].item())
+        else:             # gradients changed since (e.g. all-reduced): check them
+            self.flag.zero_()
+            for k in PARAM_GROUPS:
+                nat.check(self.lib.g6r_any_nonfinite(self.params[k].numel(), _ptr(self.grads[k]),
+                                                     _ptr(self.flag), stream))
+            bad = int(self.flag.item())
+        if bad:
             self.skipped += 1
             return
         lr_now = self.lr()

@@ -191,3 +191,27 @@ def test_data_parallel_finetune_single_rank_equals_finetune():
             np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("poison", [False, True])
+def test_trainer_backward_flags_nonfinite_gradients(poison):
+    """The backward marks non-finite gradients in counters[G6R_CNT_GRAD_NONFINITE]
+    as it writes them; DeviceTrainer.step skips Adam on it exactly like the
+    separate g6r_any_nonfinite pass over the gradient arrays (adam_step's rule)."""
+    import torch
+    from paper_2505_17338_b200 import _native as nat
+    scene, pairs = _finetune_inputs("rand400", [(0.3, 0.2, 64, 48)])
+    if poison:   # a NaN target pixel: NaN loss gradient there, NaN parameter gradients
+        cam, t = pairs[0]
+        t = np.array(t, dtype=np.float64)
+        t[20, 30, 1] = np.nan
+        pairs = [(cam, t)]
+    tr = D.DeviceTrainer(scene, pairs, total_steps=10)
+    before = {k: v.clone() for k, v in tr.params.items()}
+    tr.step(0)
+    flag = int(tr.counters[nat.CNT_GRAD_NONFINITE].item())
+    finite = all(bool(torch.isfinite(g).all()) for g in tr.grads.values())
+    assert flag == int(not finite) == int(poison)
+    assert (tr.skipped, tr.step_count) == ((1, 0) if poison else (0, 1))
+    same = all(torch.equal(before[k], tr.params[k]) for k in before)
+    assert same == poison
