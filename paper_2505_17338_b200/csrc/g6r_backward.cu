@@ -51,7 +51,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
                 const int32_t *__restrict__ last_contrib, const double *__restrict__ grad_image,
                 const int4 *__restrict__ rect, double *__restrict__ egrad_all, int64_t cap) {
     __shared__ BwdSplat s_sp[kBwdBatch];
-    __shared__ int s_orig[kBwdBatch];
+    __shared__ int s_orig[2][kBwdBatch];   // by batch parity: staged while the previous is written
     __shared__ unsigned s_mask[kBwdBatch];
     __shared__ double s_part[4][kBwdBatch][9];
     __shared__ double s_red[4][9][33];   // per-warp transpose of the 9 partials
@@ -97,26 +97,36 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
     const int64_t top = lo + s_maxlast;
     const double fx = (double)px, fy = (double)py;
     double sr = 0.0, sg = 0.0, sb = 0.0, sa = 0.0;
-    for (int64_t b1 = top; b1 > lo; b1 -= kBwdBatch) {
-        const int cnt = (int)(b1 - lo < kBwdBatch ? b1 - lo : kBwdBatch);
-        if (threadIdx.x < cnt) {   // entry j of the batch is e = b1 - 1 - j (descending)
-            const int j = threadIdx.x;
-            const int64_t e = b1 - 1 - j;
-            const unsigned m = vals[e];
-            const PayloadF64 pl = payload[m];
-            s_sp[j] = BwdSplat{pl.a.x, pl.a.y, pl.b.x, pl.b.y, pl.c.x, pl.c.y, pl.d.x, pl.d.y, pl.e.x};
-            const int4 rc = rect[m];
-            s_orig[j] = rc.x + (ty - rc.z) * rc.w + (tx - rc.y);
-            const float ex = (float)pl.e.y, ey = (float)pl.f.x;
-            const float mx = (float)pl.a.x, my = (float)pl.a.y;
-            unsigned mk = 0;
-            for (int w = 0; w < 4; ++w) {
-                const float4 bx = s_wbox[w];
-                if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) mk |= 1u << w;
-            }
-            s_mask[j] = mk;
+    // Stage the batch ending at b (entries b-1 down to b-cnt): splat rows, the
+    // entries' egrad slots, per-warp footprint masks.  `m` is this thread's
+    // entry's splat row, loaded one batch ahead (its latency hides behind the
+    // previous batch's sweep).
+    auto batch_len = [&](int64_t b) { return (int)(b - lo < kBwdBatch ? b - lo : kBwdBatch); };
+    auto fetch_row = [&](int64_t b) {
+        return (b > lo && threadIdx.x < batch_len(b)) ? vals[b - 1 - threadIdx.x] : 0u;
+    };
+    auto stage = [&](int64_t b, int buf, unsigned m) {
+        if (b <= lo || threadIdx.x >= batch_len(b)) return;
+        const int j = threadIdx.x;
+        const PayloadF64 pl = payload[m];
+        s_sp[j] = BwdSplat{pl.a.x, pl.a.y, pl.b.x, pl.b.y, pl.c.x, pl.c.y, pl.d.x, pl.d.y, pl.e.x};
+        const int4 rc = rect[m];
+        s_orig[buf][j] = rc.x + (ty - rc.z) * rc.w + (tx - rc.y);
+        const float ex = (float)pl.e.y, ey = (float)pl.f.x;
+        const float mx = (float)pl.a.x, my = (float)pl.a.y;
+        unsigned mk = 0;
+        for (int w = 0; w < 4; ++w) {
+            const float4 bx = s_wbox[w];
+            if (mx + ex >= bx.x && mx - ex <= bx.y && my + ey >= bx.z && my - ey <= bx.w) mk |= 1u << w;
         }
-        __syncthreads();
+        s_mask[j] = mk;
+    };
+    stage(top, 0, fetch_row(top));
+    unsigned m_next = fetch_row(top - kBwdBatch);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t b1 = top; b1 > lo; b1 -= kBwdBatch, buf ^= 1) {
+        const int cnt = batch_len(b1);
         unsigned hitw[kBwdWords], rowm[kBwdWords];
 #pragma unroll
         for (int q = 0; q < kBwdWords; ++q) {
@@ -210,8 +220,11 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             double v = 0.0;
             for (int w = 0; w < 4; ++w)
                 if ((s_rowm[w][j >> 5] >> (j & 31)) & 1u) v += s_part[w][j][k];
-            egrad[(int64_t)s_orig[j] * 9 + k] = v;
+            egrad[(int64_t)s_orig[buf][j] * 9 + k] = v;
         }
+        // the next batch is staged in the same phase (its buffers are not read here)
+        stage(b1 - kBwdBatch, buf ^ 1, m_next);
+        m_next = fetch_row(b1 - 2 * kBwdBatch);
         __syncthreads();
     }
 }
