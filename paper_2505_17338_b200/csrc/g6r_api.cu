@@ -643,7 +643,7 @@ int g6r_trace_dump(const char *path) {
 
 // Backward workspace: the f64 forward layout followed by the gradient buffers.
 struct BwdLayout {
-    size_t fwd, gids, rect, egrad, gsplat, final_t, last, image, total;
+    size_t fwd, gids, drawn, rect, egrad, gsplat, final_t, last, image, total;
 };
 
 static BwdLayout bwd_layout(int64_t n, int32_t width, int32_t height, int32_t tile_size, int64_t cap) {
@@ -655,6 +655,8 @@ static BwdLayout bwd_layout(int64_t n, int32_t width, int32_t height, int32_t ti
     B.fwd = 0;
     B.gids = o;
     o = align_up(o + nn * 8);
+    B.drawn = o;   // per scene row: drawn in this view (k_splat_grad_sum)
+    o = align_up(o + nn);
     B.rect = o;
     o = align_up(o + nn * 16);
     B.egrad = o;   // one 9-double row per entry and per tile band (2)
@@ -747,7 +749,8 @@ int g6r_backward_apply(const g6r_scene *scene, const g6r_camera *cam, const g6r_
     const int rc = launch_backward(
         b.vp[0], *scene, b.ws[0], counters, reinterpret_cast<double *>(base + B.final_t),
         reinterpret_cast<int32_t *>(base + B.last), grad_image,
-        reinterpret_cast<int64_t *>(base + B.gids), reinterpret_cast<double *>(base + B.egrad),
+        reinterpret_cast<int64_t *>(base + B.gids), reinterpret_cast<uint8_t *>(base + B.drawn),
+        reinterpret_cast<double *>(base + B.egrad),
         reinterpret_cast<double *>(base + B.gsplat), mu_p, mu_d, cov_raw, sh, spatial_scale,
         directional_scale, w_mode, g_mu_p, g_mu_d, g_cov_raw, g_sh, g_opacity_raw,
         (cudaStream_t)stream);

@@ -230,8 +230,13 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
 }
 
 // Zero both bands' rows of the view's entries (slots [0, entries)): rows the
-// sweep never reaches stay zero; the rest are overwritten.
-__global__ void k_zero_rows(const int64_t *counters, int64_t cap, double *__restrict__ egrad) {
+// sweep never reaches stay zero; the rest are overwritten.  Also clears the
+// per-row drawn marks (k_splat_grad_sum sets the view's drawn rows).
+__global__ void k_zero_rows(const int64_t *counters, int64_t cap, double *__restrict__ egrad,
+                            int64_t scene_rows, uint8_t *__restrict__ drawn) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < scene_rows;
+         i += (int64_t)gridDim.x * blockDim.x)
+        drawn[i] = 0;
     const int64_t e = counters[G6R_CNT_ENTRIES];
     const int64_t n = (e < cap ? e : cap) * 9;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -241,10 +246,12 @@ __global__ void k_zero_rows(const int64_t *counters, int64_t cap, double *__rest
     }
 }
 
-// g_splat[m] = sum of its entries' rows, ascending tile order (np.add.at order).
+// g_splat of drawn splat m = sum of its entries' rows, ascending tile order
+// (np.add.at order), stored at its scene row gids[m], which is marked drawn.
 __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
                                  const int64_t *counters, const double *__restrict__ egrad,
-                                 int64_t cap, double *__restrict__ gsplat) {
+                                 int64_t cap, const int64_t *__restrict__ gids,
+                                 double *__restrict__ gsplat, uint8_t *__restrict__ drawn) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t mm = counters[G6R_CNT_DRAWN];
     if (m >= mm || m >= m_total) return;
@@ -256,8 +263,10 @@ __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
     for (int64_t i = a; i < b; ++i)   // entry row = upper band + lower band
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] += egrad[i * 9 + k] + egrad[(cap + i) * 9 + k];
+    const int64_t row = gids[m];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) gsplat[m * 9 + k] = acc[k];
+    for (int k = 0; k < 9; ++k) gsplat[row * 9 + k] = acc[k];
+    drawn[row] = 1;
 }
 
 struct BwdScene {
@@ -273,17 +282,15 @@ struct BwdOut {
 #ifndef G6R_ROWS_MINB
 #define G6R_ROWS_MINB 3
 #endif
-// Chain one splat's 9 screen-space gradients to its 40 raw parameters
-// (diffrender.py:183-398, same intermediate names).
-__global__ void __launch_bounds__(128, G6R_ROWS_MINB)
-k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
-                const int64_t *__restrict__ gids, const double *__restrict__ gsplat, BwdOut out,
-                double sh_c0, double sh_c1) {
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= counters[G6R_CNT_DRAWN]) return;
-    const int64_t i = gids[m];
-    const int64_t n = scene.n;
-    const double2 *rec = reinterpret_cast<const double2 *>(scene.records);
+// Chain one drawn splat's 9 screen-space gradients gs to its 40 raw
+// parameters (diffrender.py:183-398, same intermediate names): go = g_mu_p (3),
+// g_mu_d (3), g_cov_raw (21, from the row's raw cov parameters `raw`), g_sh
+// (12), g_opacity_raw (1).
+constexpr int kGradOut = 40;
+__device__ __forceinline__ void chain_row(const ViewParams &vp, const BwdScene &sc,
+                                          const double2 *__restrict__ rec, int64_t n, int64_t i,
+                                          const double *raw, const double *gs, double sh_c0,
+                                          double sh_c1, double *go) {
     double r[G6R_REC_DOUBLES];
 #pragma unroll
     for (int c = 0; c < G6R_REC_COLUMNS; ++c) {
@@ -350,7 +357,6 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
     const double ia = cov_c * inv_det, ib = -cov_b * inv_det, ic = cov_a * inv_det;
 
     // --- reverse sweep ------------------------------------------------------
-    const double *gs = gsplat + m * 9;
     const double g_u = gs[0], g_v = gs[1], g_ia = gs[2], g_ib = gs[3], g_ic = gs[4];
     const double g_col[3] = {gs[5], gs[6], gs[7]};
     const double g_alpha = gs[8];
@@ -428,7 +434,6 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
     for (int a = 0; a < 6; ++a)
         for (int b = 0; b < 6; ++b) L[a][b] = 0.0;
     const double scale[6] = {sc.ss[0], sc.ss[1], sc.ss[2], sc.ds, sc.ds, sc.ds};
-    const double *raw = sc.cov_raw + 21 * i;
     for (int k = 0; k < 6; ++k) L[k][k] = scale[k] * exp(raw[k]);
 #pragma unroll
     for (int k = 0; k < 15; ++k) L[tril_i(k)][tril_j(k)] = tanh(raw[6 + k]);
@@ -492,26 +497,63 @@ k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
     }
     for (int k = 0; k < 3; ++k) g_v3[k] += g_d[k];
     const double vdot = v[0] * g_v3[0] + v[1] * g_v3[1] + v[2] * g_v3[2];
-    double g_mp[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
-        g_mp[k] = g_madj[k] + (g_v3[k] - v[k] * vdot) * inv_dist;
-        out.g_mu_p[3 * i + k] = g_mp[k];
-        out.g_mu_d[3 * i + k] = -g_d[k];
+        go[k] = g_madj[k] + (g_v3[k] - v[k] * vdot) * inv_dist;
+        go[3 + k] = -g_d[k];
     }
-    for (int k = 0; k < 21; ++k) out.g_cov_raw[21 * i + k] = g_raw[k];
-    for (int k = 0; k < 12; ++k) out.g_sh[12 * i + k] = g_shv[k];
-    out.g_opacity_raw[i] = g_opacity_raw;
-    // non-finite check of the 40 values written (the rows not written are
-    // zeros): the largest exponent field, all-ones only for inf / nan
-    unsigned ex = (unsigned)__double2hiint(g_opacity_raw) & 0x7ff00000u;
-    auto acc = [&](double x) { ex = max(ex, (unsigned)__double2hiint(x) & 0x7ff00000u); };
-    for (int k = 0; k < 3; ++k) {
-        acc(g_mp[k]);
-        acc(g_d[k]);
-    }
-    for (int k = 0; k < 21; ++k) acc(g_raw[k]);
-    for (int k = 0; k < 12; ++k) acc(g_shv[k]);
+#pragma unroll
+    for (int k = 0; k < 21; ++k) go[6 + k] = g_raw[k];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) go[27 + k] = g_shv[k];
+    go[39] = g_opacity_raw;
+}
+
+// One thread per scene row, 128 consecutive rows per CTA: the rows' AoS
+// inputs (cov_raw, 21 doubles; the splat's screen-space gradient, 9) are
+// staged through shared memory with coalesced loads and the 40 outputs leave
+// the same way, so every global access is a contiguous block of the CTA's
+// rows (per-thread strided rows cost 4x the L1 sectors).  Rows the view did
+// not draw get exact zeros (no memset of the gradient arrays).
+constexpr int kRowsIn = 30;
+__global__ void __launch_bounds__(128, G6R_ROWS_MINB)
+k_backward_rows(ViewParams vp, BwdScene sc, g6r_scene scene, int64_t *counters,
+                const uint8_t *__restrict__ drawn, const double *__restrict__ gsplat, BwdOut out,
+                double sh_c0, double sh_c1) {
+    __shared__ double s_io[128 * kRowsIn];
+    const int64_t n = scene.n;
+    const int64_t i0 = (int64_t)blockIdx.x * 128;
+    const int rows = n - i0 < 128 ? (int)(n - i0) : 128;
+    const int t = threadIdx.x;
+    for (int k = t; k < rows * 21; k += 128) s_io[(k / 21) * kRowsIn + k % 21] = sc.cov_raw[i0 * 21 + k];
+    for (int k = t; k < rows * 9; k += 128) s_io[(k / 9) * kRowsIn + 21 + k % 9] = gsplat[i0 * 9 + k];
+    __syncthreads();
+    double go[kGradOut];
+#pragma unroll
+    for (int k = 0; k < kGradOut; ++k) go[k] = 0.0;
+    if (t < rows && drawn[i0 + t])
+        chain_row(vp, sc, reinterpret_cast<const double2 *>(scene.records), n, i0 + t,
+                  s_io + t * kRowsIn, s_io + t * kRowsIn + 21, sh_c0, sh_c1, go);
+    // non-finite check of the row's outputs: the largest exponent field,
+    // all-ones only for inf / nan
+    unsigned ex = 0;
+#pragma unroll
+    for (int k = 0; k < kGradOut; ++k) ex = max(ex, (unsigned)__double2hiint(go[k]) & 0x7ff00000u);
     if (ex == 0x7ff00000u) counters[G6R_CNT_GRAD_NONFINITE] = 1;
+    __syncthreads();   // inputs consumed: s_io stages the outputs, one array at a time
+#define G6R_PUT_ROWS(dst, off, w)                                                   \
+    {                                                                               \
+        _Pragma("unroll") for (int k = 0; k < (w); ++k) s_io[t * (w) + k] = go[(off) + k]; \
+        __syncthreads();                                                            \
+        for (int k = t; k < rows * (w); k += 128) (dst)[i0 * (w) + k] = s_io[k];    \
+        __syncthreads();                                                            \
+    }
+    G6R_PUT_ROWS(out.g_cov_raw, 6, 21)
+    G6R_PUT_ROWS(out.g_sh, 27, 12)
+    G6R_PUT_ROWS(out.g_mu_p, 0, 3)
+    G6R_PUT_ROWS(out.g_mu_d, 3, 3)
+#undef G6R_PUT_ROWS
+    if (t < rows) out.g_opacity_raw[i0 + t] = go[39];
 }
 
 static const double kShC0b = 0.28209479177387814;
@@ -519,30 +561,27 @@ static const double kShC1b = 0.4886025119029199;
 
 int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspace &ws,
                     int64_t *counters, const double *final_t, const int32_t *last,
-                    const double *grad_image, const int64_t *gids, double *egrad, double *gsplat,
+                    const double *grad_image, const int64_t *gids, uint8_t *drawn, double *egrad,
+                    double *gsplat,
                     const double *mu_p, const double *mu_d, const double *cov_raw, const double *sh,
                     const double *ss, double ds, int w_mode, double *g_mu_p, double *g_mu_d,
                     double *g_cov_raw, double *g_sh, double *g_opacity_raw, cudaStream_t st) {
     if (vp.tile_size != 16) return G6R_EINVAL;
     const int64_t n = scene.n;
-    cudaMemsetAsync(g_mu_p, 0, (size_t)n * 3 * sizeof(double), st);
-    cudaMemsetAsync(g_mu_d, 0, (size_t)n * 3 * sizeof(double), st);
-    cudaMemsetAsync(g_cov_raw, 0, (size_t)n * 21 * sizeof(double), st);
-    cudaMemsetAsync(g_sh, 0, (size_t)n * 12 * sizeof(double), st);
-    cudaMemsetAsync(g_opacity_raw, 0, (size_t)n * sizeof(double), st);
     cudaMemsetAsync(counters + G6R_CNT_GRAD_NONFINITE, 0, sizeof(int64_t), st);
     if (n == 0) return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
-    k_zero_rows<<<148 * 4, 256, 0, st>>>(counters, ws.entry_capacity, egrad);
+    k_zero_rows<<<148 * 4, 256, 0, st>>>(counters, ws.entry_capacity, egrad, n, drawn);
     k_composite_bwd<<<vp.tiles_x * vp.tiles_y * 2, 128, 0, st>>>(
         vp, static_cast<const PayloadF64 *>(ws.payload), ws.vals[0], ws.vals[1], ws.internal,
         ws.tile_starts, final_t, last, grad_image, ws.splat_rect, egrad, ws.entry_capacity);
     trace_mark("composite_bwd", st);
     const unsigned grid = (unsigned)ceil_div(n, 128);
-    k_splat_grad_sum<<<grid, 128, 0, st>>>(n, ws.splat_rect, counters, egrad, ws.entry_capacity, gsplat);
+    k_splat_grad_sum<<<grid, 128, 0, st>>>(n, ws.splat_rect, counters, egrad, ws.entry_capacity, gids,
+                                           gsplat, drawn);
     trace_mark("splat_grad_sum", st);
     BwdScene sc{mu_p, mu_d, cov_raw, sh, {ss[0], ss[1], ss[2]}, ds, w_mode};
     BwdOut out{g_mu_p, g_mu_d, g_cov_raw, g_sh, g_opacity_raw};
-    k_backward_rows<<<grid, 128, 0, st>>>(vp, sc, scene, counters, gids, gsplat, out, kShC0b, kShC1b);
+    k_backward_rows<<<grid, 128, 0, st>>>(vp, sc, scene, counters, drawn, gsplat, out, kShC0b, kShC1b);
     trace_mark("backward_rows", st);
     return cudaGetLastError() == cudaSuccess ? G6R_OK : G6R_ECUDA;
 }

@@ -142,7 +142,7 @@ int launch_stage2(int64_t n, const double *view, const double *mean_adj, const d
 
 int launch_backward(const ViewParams &vp, const g6r_scene &scene, const Workspace &ws,
                     int64_t *counters, const double *final_t, const int32_t *last,
-                    const double *grad_image, const int64_t *gids, double *egrad, double *gsplat,
+                    const double *grad_image, const int64_t *gids, uint8_t *drawn, double *egrad, double *gsplat,
                     const double *mu_p, const double *mu_d, const double *cov_raw, const double *sh,
                     const double *ss, double ds, int w_mode, double *g_mu_p, double *g_mu_d,
                     double *g_cov_raw, double *g_sh, double *g_opacity_raw, cudaStream_t st);
