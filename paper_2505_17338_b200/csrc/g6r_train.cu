@@ -69,33 +69,58 @@ __global__ void k_products(const double *__restrict__ x, const double *__restric
 
 // 1-D correlation with the window along one axis of `planes` (h, w) planes.
 // valid: out length n - 10; full: n + 10 (zero padding, the adjoint).
-// grid (column blocks, output rows, channels x planes): no index division in
-// the pixel loop; the taps are summed in order (k ascending)
-__global__ void k_corr1d(const double *__restrict__ in, double *__restrict__ out, int planes, int h,
-                         int w, int axis, int full, int64_t cs) {
-    const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
-    const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
+// grid (column blocks of 128, row blocks of kCorrRows, channels x planes).
+// The CTA stages the input window of its output tile through shared memory
+// with coalesced loads (zeros outside the image), then every thread sums its
+// column's taps for kCorrRows output rows from shared memory: each input is
+// read from L2 about once instead of once per tap.  Same taps, same order
+// (k ascending), out-of-image taps skipped as before: identical bits.
+constexpr int kCorrCols = 128, kCorrRows = 16;
+template <int kAxis>
+__global__ void __launch_bounds__(kCorrCols)
+k_corr1d(const double *__restrict__ in, double *__restrict__ out, int planes, int h, int w, int full,
+         int64_t cs) {
+    constexpr int SH = kAxis == 0 ? kCorrRows + kWin - 1 : kCorrRows;   // staged rows
+    constexpr int SW = kAxis == 0 ? kCorrCols : kCorrCols + kWin - 1;   // staged columns
+    __shared__ double s_in[SH * SW];
+    const int oh = kAxis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
+    const int ow = kAxis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
     const int shift = full ? kWin - 1 : 0;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
     const int c = blockIdx.z / planes, p = blockIdx.z - c * planes;
-    if (j >= ow || i >= oh) return;
-    in += c * cs;
-    out += c * cs;
-    const double *src = in + (int64_t)p * h * w;
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < kWin; ++k) {
-        const int ii = axis == 0 ? i + k - shift : i;
-        const int jj = axis == 1 ? j + k - shift : j;
-        if (ii >= 0 && ii < h && jj >= 0 && jj < w) s += c_win[k] * src[(int64_t)ii * w + jj];
+    const double *src = in + c * cs + (int64_t)p * h * w;
+    double *dst = out + c * cs + (int64_t)p * oh * ow;
+    const int j0 = blockIdx.x * kCorrCols, i0 = blockIdx.y * kCorrRows;
+    // input window origin: (i0 - shift, j0) vertically, (i0, j0 - shift) horizontally
+    const int ri = kAxis == 0 ? i0 - shift : i0, rj = kAxis == 1 ? j0 - shift : j0;
+    for (int q = threadIdx.x; q < SH * SW; q += kCorrCols) {
+        const int a = q / SW, b = q - a * SW;
+        const int ii = ri + a, jj = rj + b;
+        s_in[q] = (ii >= 0 && ii < h && jj >= 0 && jj < w) ? src[(int64_t)ii * w + jj] : 0.0;
     }
-    out[((int64_t)p * oh + i) * ow + j] = s;
+    __syncthreads();
+    const int j = j0 + threadIdx.x;
+    if (j >= ow) return;
+    for (int r = 0; r < kCorrRows; ++r) {
+        const int i = i0 + r;
+        if (i >= oh) break;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+            const int ii = kAxis == 0 ? i + k - shift : i;
+            const int jj = kAxis == 1 ? j + k - shift : j;
+            if (ii >= 0 && ii < h && jj >= 0 && jj < w)
+                s += c_win[k] * (kAxis == 0 ? s_in[(r + k) * SW + threadIdx.x]
+                                            : s_in[r * SW + threadIdx.x + k]);
+        }
+        dst[(int64_t)i * ow + j] = s;
+    }
 }
 
 static dim3 corr_grid(int planes, int h, int w, int axis, int full) {
     const int oh = axis == 0 ? (full ? h + kWin - 1 : h - kWin + 1) : h;
     const int ow = axis == 1 ? (full ? w + kWin - 1 : w - kWin + 1) : w;
-    return dim3((unsigned)((ow + 127) / 128), (unsigned)std::max(oh, 1), (unsigned)(3 * planes));
+    return dim3((unsigned)((ow + kCorrCols - 1) / kCorrCols),
+                (unsigned)std::max((oh + kCorrRows - 1) / kCorrRows, 1), (unsigned)(3 * planes));
 }
 
 // SSIM window maps (_ssim.py:66-84) from the 5 correlated statistics
@@ -460,8 +485,8 @@ static void loss_launch(const double *pred, const double *tgt, int tc, int h, in
             const int hv = hj - kWin + 1, wv = wj - kWin + 1;
             const int64_t nv = (int64_t)hv * wv;
             k_products<<<dim3(grid_for(hwj), 3), 256, 0, st>>>(xs[j], ys[j], hwj, stats, cs);
-            k_corr1d<<<corr_grid(5, hj, wj, 0, 0), 128, 0, st>>>(stats, tmp, 5, hj, wj, 0, 0, cs);
-            k_corr1d<<<corr_grid(5, hv, wj, 1, 0), 128, 0, st>>>(tmp, stats, 5, hv, wj, 1, 0, cs);
+            k_corr1d<0><<<corr_grid(5, hj, wj, 0, 0), kCorrCols, 0, st>>>(stats, tmp, 5, hj, wj, 0, cs);
+            k_corr1d<1><<<corr_grid(5, hv, wj, 1, 0), kCorrCols, 0, st>>>(tmp, stats, 5, hv, wj, 0, cs);
             k_ssim_maps<<<dim3(grid_for(nv), 3), 256, 0, st>>>(stats, nv, mp[j], cs);
             if (j == ns - 1) dsum(mp[j] + 4 * nv, mp[j] + 5 * nv, nv, 3, cs, part, chan + j, kChanStride, st);
             else dsum(mp[j] + 5 * nv, nullptr, nv, 3, cs, part, chan + j, kChanStride, st);
@@ -487,8 +512,8 @@ static void loss_launch(const double *pred, const double *tgt, int tc, int h, in
             }
             k_ssim_bwd_maps<<<dim3(grid_for(nv), 3), 256, 0, st>>>(mp[j], nv, chan + 6 + j, kChanStride,
                                                                   j == ns - 1, gm, cs);
-            k_corr1d<<<corr_grid(3, hv, wv, 0, 1), 128, 0, st>>>(gm, tmp, 3, hv, wv, 0, 1, cs);
-            k_corr1d<<<corr_grid(3, hj, wv, 1, 1), 128, 0, st>>>(tmp, adj, 3, hj, wv, 1, 1, cs);
+            k_corr1d<0><<<corr_grid(3, hv, wv, 0, 1), kCorrCols, 0, st>>>(gm, tmp, 3, hv, wv, 1, cs);
+            k_corr1d<1><<<corr_grid(3, hj, wv, 1, 1), kCorrCols, 0, st>>>(tmp, adj, 3, hj, wv, 1, cs);
             k_ssim_bwd_combine<<<dim3(grid_for(hwj), 3), 256, 0, st>>>(adj, xs[j], ys[j], hwj, g, cs);
         }
         // grad_rgb -= lambda_ssim * g_ms, with g_ms averaged over channels
