@@ -522,9 +522,9 @@ static void loss_launch(const double *pred, const double *tgt, int tc, int h, in
     k_loss_parts<<<1, 32, 0, st>>>(scal, lambda_ssim > 0.0, lambda_l1, lambda_ssim, (double)(hw * 3));
 }
 
-// The ~150 small kernels of one loss evaluation are captured once per
+// The ~75 small kernels of one loss evaluation are captured once per
 // (device, workspace, image size, channels, weights) into a CUDA graph on a
-// private stream and replayed: one launch instead of ~150, same kernels in the
+// private stream and replayed: one launch instead of ~75, same kernels in the
 // same order, hence the same bits.  The caller's buffers are copied to / from
 // fixed workspace regions around the replay.
 struct LossGraph {
