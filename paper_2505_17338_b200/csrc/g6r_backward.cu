@@ -220,6 +220,7 @@ k_composite_bwd(ViewParams vp, const PayloadF64 *__restrict__ payload,
             double v = 0.0;
             for (int w = 0; w < 4; ++w)
                 if ((s_rowm[w][j >> 5] >> (j & 31)) & 1u) v += s_part[w][j][k];
+            G6R_CHECK(s_orig[buf][j] >= 0 && s_orig[buf][j] < cap);
             egrad[(int64_t)s_orig[buf][j] * 9 + k] = v;
         }
         // the next batch is staged in the same phase (its buffers are not read here)
@@ -264,6 +265,7 @@ __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] += egrad[i * 9 + k] + egrad[(cap + i) * 9 + k];
     const int64_t row = gids[m];
+    G6R_CHECK(row >= 0 && row < m_total && a <= b && b <= cap);
 #pragma unroll
     for (int k = 0; k < 9; ++k) gsplat[row * 9 + k] = acc[k];
     drawn[row] = 1;
