@@ -255,7 +255,9 @@ __global__ void k_splat_grad_sum(int64_t m_total, const int4 *__restrict__ rect,
                                  double *__restrict__ gsplat, uint8_t *__restrict__ drawn) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t mm = counters[G6R_CNT_DRAWN];
-    if (m >= mm || m >= m_total) return;
+    // an overflowed forward (entries beyond the capacity, empty runs) has no
+    // entry rows: every splat stays undrawn, so every gradient row is zero
+    if (counters[G6R_CNT_OVERFLOW] || m >= mm || m >= m_total) return;
     const int64_t a = rect[m].x;
     const int64_t b = m + 1 < mm ? (int64_t)rect[m + 1].x : counters[G6R_CNT_ENTRIES];
     double acc[9];

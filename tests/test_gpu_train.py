@@ -215,3 +215,20 @@ def test_trainer_backward_flags_nonfinite_gradients(poison):
     assert (tr.skipped, tr.step_count) == ((1, 0) if poison else (0, 1))
     same = all(torch.equal(before[k], tr.params[k]) for k in before)
     assert same == poison
+
+
+def test_trainer_entry_overflow_is_redone():
+    """A forward that overflows the entry capacity (empty runs) is detected at
+    the step's read-back; the capacity grows and the view is rendered again:
+    the same loss row and parameters as a step that never overflowed."""
+    import torch
+    scene, pairs = _finetune_inputs("rand400", [(0.3, 0.2, 64, 48), (1.1, -0.2, 48, 64)])
+    a = D.DeviceTrainer(scene, pairs, total_steps=10)
+    b = D.DeviceTrainer(scene, pairs, total_steps=10)
+    b.cap = 16   # far below the view's entries
+    for k in range(3):
+        ra, rb = a.step(k % 2), b.step(k % 2)
+        assert ra == rb, k
+    assert b.cap > 16
+    for key in D.PARAM_GROUPS:
+        assert torch.equal(a.params[key], b.params[key]), key
