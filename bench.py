@@ -129,7 +129,6 @@ class ClockSampler:
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "50", "-i", str(self.gpu), "-f", self.path],
                 stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
-            time.sleep(0.15)
         except Exception:
             self.proc = None
 
@@ -458,6 +457,17 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     clocks.start()
+    # while nvidia-smi starts up, keep the GPU busy with the same (untimed)
+    # call: an idle wait here lets the clocks drop and the sampler's start-up
+    # land in the timed region (measured: 4.1-4.5 ms instead of 3.97 ms for
+    # the 20 views)
+    t_busy = time.perf_counter() + 0.4
+    while time.perf_counter() < t_busy:
+        raster.render_views(scene, cams, config=cfg, capacity=cap, out=images,
+                            concurrency=args.concurrency)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     ev0.record()
     _, counters = raster.render_views(scene, cams, config=cfg, capacity=cap, out=images,
