@@ -203,7 +203,7 @@ void g6r_profiler_reset(g6r_profiler *prof);
 int g6r_profiler_read(g6r_profiler *prof, double *stage_ms, int32_t *views);
 
 /* Render `count` views of one scene (same image size) into frames[k], in
- * batches of `batch` views (1..32): every stage kernel processes a whole batch
+ * batches of `batch` views (1..16): every stage kernel processes a whole batch
  * per launch (grid = work x views), so one view's long tile runs overlap the
  * other views' work and the projection shares the record stream through L2.
  * The workspace must hold batch x g6r_workspace_bytes(...).  When it holds

@@ -14,7 +14,7 @@
 
 namespace g6r {
 
-constexpr int kMaxBatch = 32;
+constexpr int kMaxBatch = 16;
 
 // Workspace carve-up for one view (see g6r_api.cu::layout).
 struct Workspace {

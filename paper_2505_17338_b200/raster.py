@@ -527,7 +527,7 @@ def render_device(scene, camera, group_mask=None, config: RenderConfig = DEFAULT
 
 
 DEFAULT_CONCURRENCY = 16  # views per batched launch (g6r_render_views)
-MAX_BATCH = 32            # kMaxBatch in csrc/g6r_internal.h
+MAX_BATCH = 16            # kMaxBatch in csrc/g6r_internal.h
 PIPELINE_LANES = int(os.environ.get("G6R_LANES", "2"))   # streams batches alternate over (<= 4)
 # render_batch writing the pinned host images directly from the compositor
 # (G6R_ZERO_COPY=1).  Off by default: measured at cfg3 (20 views), the PCIe
@@ -602,14 +602,22 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     ws = torch.empty(max(per * slots * lanes, 256), dtype=torch.uint8, device=dev)
     cam_arr = (nat.Camera * V)(*[_camera_struct(c) for c in cams])
     bg = (ctypes.c_double * 3)(*[float(c) for c in background])
-    frames = (nat.Frame * V)(*[nat.Frame(images[v].data_ptr() if images is not None else 0, 0, 0,
-                                         counters[v].data_ptr(),
-                                         entry_splat[v].data_ptr() if entry_splat is not None else 0,
-                                         tile_starts[v].data_ptr() if tile_starts is not None else 0,
-                                         rgba8[v].data_ptr() if rgba8 is not None else 0, bg,
-                                         host_out[v].data_ptr() if host_out is not None else 0,
-                                         host_rgba8[v].data_ptr() if host_rgba8 is not None else 0)
-                               for v in range(V)])
+    # per-view addresses by stride arithmetic on the contiguous outputs (a
+    # tensor index per view costs a few microseconds of host time, and the
+    # host time before the first launch is GPU idle time)
+    if images is not None and not images.is_contiguous():
+        raise InvalidParameterError("out must be a contiguous (V, H, W, 4) tensor")
+
+    def rows(t):
+        if t is None:
+            return lambda v: 0
+        base, step = t.data_ptr(), t.stride(0) * t.element_size()
+        return lambda v: base + v * step
+
+    p_img, p_cnt, p_es, p_ts = rows(images), rows(counters), rows(entry_splat), rows(tile_starts)
+    p_rgba, p_hout, p_hrgba = rows(rgba8), rows(host_out), rows(host_rgba8)
+    frames = (nat.Frame * V)(*[nat.Frame(p_img(v), 0, 0, p_cnt(v), p_es(v), p_ts(v), p_rgba(v), bg,
+                                         p_hout(v), p_hrgba(v)) for v in range(V)])
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
                                           _ptr(ws), per * slots * lanes, cap, frames, slots,
