@@ -335,3 +335,18 @@ def test_train_entry_points_reject_bad_arguments():
                                   None) == nat.G6R_EINVAL
     assert lib.g6r_decode_records(4, ctypes.c_void_p(257), dummy, dummy, dummy, dummy, dummy,
                                   dummy, dummy, None) == nat.G6R_EINVAL
+
+
+def test_camera_array_matches_camera_structs():
+    """render_views' column-filled camera array is byte for byte the
+    g6r_camera structs _camera_struct builds one by one."""
+    import ctypes
+    from paper_2505_17338_b200 import raster, scenes
+    from paper_2505_17338_b200 import _native as nat
+    cams = [scenes.orbit_camera(azimuth=0.37 * k, elevation=0.1 * k - 0.2, width=96 + k, height=64,
+                                fov_y=0.5 + 0.1 * k) for k in range(5)]
+    a = raster._camera_array(cams)
+    arr = (nat.Camera * len(cams)).from_buffer(a)
+    assert ctypes.sizeof(nat.Camera) == a.dtype.itemsize
+    for k, c in enumerate(cams):
+        assert bytes(arr[k]) == bytes(raster._camera_struct(c)), k
