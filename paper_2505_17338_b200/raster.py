@@ -435,6 +435,12 @@ def _camera_array(cams):
     return a
 
 
+_FRAME_DTYPE = np.dtype([("image", "<u8"), ("final_t", "<u8"), ("last_contrib", "<u8"),
+                         ("counters", "<u8"), ("entry_splat", "<u8"), ("tile_starts", "<u8"),
+                         ("rgba8", "<u8"), ("background", "<f8", (3,)), ("host_image", "<u8"),
+                         ("host_rgba8", "<u8")])   # g6r_frame (g6r.h)
+
+
 def _tiles(camera, tile_size):
     tx = (int(camera.width) + tile_size - 1) // tile_size
     ty = (int(camera.height) + tile_size - 1) // tile_size
@@ -624,23 +630,20 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
     ws = torch.empty(max(per * slots * lanes, 256), dtype=torch.uint8, device=dev)
     cam_np = _camera_array(cams)
     cam_arr = (nat.Camera * V).from_buffer(cam_np)
-    bg = (ctypes.c_double * 3)(*[float(c) for c in background])
-    # per-view addresses by stride arithmetic on the contiguous outputs (a
-    # tensor index per view costs a few microseconds of host time, and the
-    # host time before the first launch is GPU idle time)
+    # per-view frames with addresses by stride arithmetic on the contiguous
+    # outputs (a tensor index or a ctypes struct per view costs microseconds
+    # of host time, and the host time before the first launch is GPU idle)
     if images is not None and not images.is_contiguous():
         raise InvalidParameterError("out must be a contiguous (V, H, W, 4) tensor")
-
-    def rows(t):
-        if t is None:
-            return lambda v: 0
-        base, step = t.data_ptr(), t.stride(0) * t.element_size()
-        return lambda v: base + v * step
-
-    p_img, p_cnt, p_es, p_ts = rows(images), rows(counters), rows(entry_splat), rows(tile_starts)
-    p_rgba, p_hout, p_hrgba = rows(rgba8), rows(host_out), rows(host_rgba8)
-    frames = (nat.Frame * V)(*[nat.Frame(p_img(v), 0, 0, p_cnt(v), p_es(v), p_ts(v), p_rgba(v), bg,
-                                         p_hout(v), p_hrgba(v)) for v in range(V)])
+    fr = np.zeros(V, _FRAME_DTYPE)
+    idx = np.arange(V, dtype=np.uint64)
+    for field, t in (("image", images), ("counters", counters), ("entry_splat", entry_splat),
+                     ("tile_starts", tile_starts), ("rgba8", rgba8), ("host_image", host_out),
+                     ("host_rgba8", host_rgba8)):
+        if t is not None:
+            fr[field] = np.uint64(t.data_ptr()) + idx * np.uint64(t.stride(0) * t.element_size())
+    fr["background"] = [float(c) for c in background]
+    frames = (nat.Frame * V).from_buffer(fr)
     sc = prep.scene_struct()
     nat.check(nat.load().g6r_render_views(ctypes.byref(sc), bits, cam_arr, V, ctypes.byref(cfg),
                                           _ptr(ws), per * slots * lanes, cap, frames, slots,

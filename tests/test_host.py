@@ -350,3 +350,18 @@ def test_camera_array_matches_camera_structs():
     assert ctypes.sizeof(nat.Camera) == a.dtype.itemsize
     for k, c in enumerate(cams):
         assert bytes(arr[k]) == bytes(raster._camera_struct(c)), k
+
+
+def test_frame_array_layout_matches_g6r_frame():
+    """render_views' numpy frame records have g6r_frame's size and field
+    offsets (the ctypes mirror of g6r.h)."""
+    import ctypes
+    from paper_2505_17338_b200 import raster
+    from paper_2505_17338_b200 import _native as nat
+    dt = raster._FRAME_DTYPE
+    assert dt.itemsize == ctypes.sizeof(nat.Frame)
+    for name, _ in nat.Frame._fields_:
+        assert dt.fields[name][1] == getattr(nat.Frame, name).offset, name
+    assert raster._CAMERA_DTYPE.itemsize == ctypes.sizeof(nat.Camera)
+    for name, _ in nat.Camera._fields_:
+        assert raster._CAMERA_DTYPE.fields[name][1] == getattr(nat.Camera, name).offset, name
