@@ -614,7 +614,11 @@ def run_b200(args):
                        "l2": "inputs larger than L2: the 352 MB of prepared records are read "
                              "once per batch launch (its views share them through L2) and every "
                              "view's ~110 MB of sort/partition/payload scratch is rewritten; "
-                             "no explicit flush between timed views"},
+                             "no explicit flush between timed views",
+                       "timing": "one render_views call over the K views between CUDA events "
+                                 "on the render stream (host launch time included), after the W "
+                                 "warm-up views and 0.4 s of the same untimed call while the "
+                                 "clock sampler starts"},
             "gaussians_per_s": views_per_s * n,
             "stage_ms_per_view": {k: v / max(nviews, 1) for k, v in stage_ms.items()},
             "mean_drawn": float(M.mean()), "mean_entries": float(E.mean()),
