@@ -623,6 +623,11 @@ def render_views(scene, cameras, group_mask=None, config: RenderConfig = DEFAULT
                 or not t.is_contiguous() or not t.is_pinned():
             raise InvalidParameterError(f"{name} must be a pinned contiguous CPU tensor shaped like the output")
     slots = max(1, min(int(concurrency), MAX_BATCH, V))
+    if pipeline and profiler is None and 4 <= V <= slots:
+        # one batch would leave nothing to overlap: two half batches pipelined
+        # on two streams instead (measured 16 views at 512^2 4943 -> 4962
+        # views/s, 12 at 1024^2 2751 -> 2826)
+        slots = (V + 1) // 2
     tx, ty = _tiles(cams[0], cfg.tile_size)
     per = nat.load().g6r_workspace_bytes(prep.n, tx * ty, cap, cfg.precision)
     # n batches' worth of workspace pipelines consecutive batches on n streams
